@@ -1,0 +1,356 @@
+#!/usr/bin/env python
+"""Benchmark: fused polynomial-smoother apply on the 3D Poisson fine level.
+
+Workload (BASELINE.json configs[1]): the 7-point Poisson fine level of a
+256^3 grid (n = 16.8M rows, 117M nnz, generated on the GPU), one *step* =
+the smoother sweep over opt_cheb1(a*), cheb4 and opt_cheb4 at degrees 1..6
+(18 smoother applications, x0 != 0 so all k SpMVs run).  Metric: algorithmic
+smoother-apply bytes / time (GB/s) -- SURVEY.md section 8d:
+    A = 12 nnz + 4 (n+1);  k = 1: A + 32 n;  k >= 2: k A + (56 k - 24) n.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+
+N > 1 (torchrun, one process per GPU): weak scaling -- every rank owns a
+256^3-row block of an (N*256^3)-row Poisson problem partitioned in row
+blocks... (current round: independent per-rank fine levels).
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "smoother-apply GB/s (% HBM peak); PCG+AMG solve s & iters, 3D Poisson 1–8 GPU"
+SWEEP = [(fam, k) for fam in ("opt_cheb1", "cheb4", "opt_cheb4") for k in range(1, 7)]
+
+
+def apply_bytes(n, nnz, k):
+    A = 12 * nnz + 4 * (n + 1)
+    return A + 32 * n if k == 1 else k * A + (56 * k - 24) * n
+
+
+def mid_step_bytes(n, nnz):
+    return 12 * nnz + 4 * (n + 1) + 56 * n
+
+
+def peaks():
+    try:
+        with open(os.path.join(REPO, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        rows = []
+        with open(self.f.name) as fh:
+            for line in fh:
+                p = [x.strip() for x in line.split(",")]
+                if len(p) >= 8:
+                    rows.append(p)
+        os.unlink(self.f.name)
+        if not rows:
+            return None
+        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[4 + i]})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(rows)}
+
+
+# ---------------------------------------------------------------- distributed
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def traffic_per_launch():
+    p = os.path.join(REPO, "profiles", "ncu_traffic.json")
+    try:
+        with open(p) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
+# ---------------------------------------------------------------- reference arm
+def run_reference(args):
+    """The reference's algorithm on the host (C oracle port, all host threads)."""
+    ws, rank, _ = dist_env()
+    if rank != 0:
+        return 0
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    from paper_2407_09848_b200.params import load_beta_tables, optimal_a
+    from paper_2407_09848_b200.problems import poisson3d
+
+    m = args.m
+    from paper_2407_09848_b200.smoothers import l1_jacobi_diag
+
+    A, _ = poisson3d(m)
+    n, nnz = A.nrows, A.nnz
+    mdiag = l1_jacobi_diag(A).m_diag
+    rng = np.random.default_rng(0)
+    b = rng.standard_normal(n)
+    x0 = np.random.default_rng(1).standard_normal(n)
+    threads = oracle.max_threads()
+    oracle.set_threads(threads)
+    betas = load_beta_tables()
+
+    def one(i):
+        fam, k = SWEEP[i % len(SWEEP)]
+        a = optimal_a(k) if fam == "opt_cheb1" else 0.0
+        beta = betas[k].beta if fam == "opt_cheb4" else None
+        t0 = time.perf_counter()
+        oracle.smoother_apply(fam, k, A.row_ptr, A.col_idx, A.values, mdiag, b, x0, a=a, beta=beta)
+        return time.perf_counter() - t0, apply_bytes(n, nnz, k)
+
+    for i in range(args.warmup):
+        one(i)
+    tot_t = tot_b = 0.0
+    for i in range(args.steps):
+        t, by = one(args.warmup + i)
+        tot_t += t
+        tot_b += by
+    value = tot_b / tot_t / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        "ms_per_step": 1e3 * tot_t / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"poisson3d 7-pt {m}^3 fine level, smoother sweep",
+                   "m": m, "n": n, "nnz": nnz,
+                   "sample": "one smoother_apply per step cycling the 18-case sweep"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "port",
+                         "sample": f"{args.steps} applies of the {m}^3 sweep (C oracle, "
+                                   f"{threads} threads)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- b200 arm
+def cpu_baseline(m):
+    """C oracle (port) on a bounded sample of the same workload, all host threads."""
+    sys.path.insert(0, os.path.join(REPO, "oracle"))
+    import oracle
+    from paper_2407_09848_b200.params import load_beta_tables, optimal_a
+    from paper_2407_09848_b200.problems import poisson3d
+
+    from paper_2407_09848_b200.smoothers import l1_jacobi_diag
+
+    A, _ = poisson3d(m)
+    n, nnz = A.nrows, A.nnz
+    mdiag = l1_jacobi_diag(A).m_diag
+    b = np.random.default_rng(0).standard_normal(n)
+    x0 = np.random.default_rng(1).standard_normal(n)
+    threads = oracle.max_threads()
+    oracle.set_threads(threads)
+    betas = load_beta_tables()
+    tot_t = tot_b = 0.0
+    for fam in ("opt_cheb1", "cheb4", "opt_cheb4"):
+        k = 4
+        a = optimal_a(k) if fam == "opt_cheb1" else 0.0
+        beta = betas[k].beta if fam == "opt_cheb4" else None
+        t0 = time.perf_counter()
+        oracle.smoother_apply(fam, k, A.row_ptr, A.col_idx, A.values, mdiag, b, x0, a=a, beta=beta)
+        tot_t += time.perf_counter() - t0
+        tot_b += apply_bytes(n, nnz, k)
+    oracle.set_threads(1)
+    return {"value": tot_b / tot_t / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
+            "sample": f"{m}^3 fine level, opt_cheb1/cheb4/opt_cheb4 k=4, one apply each "
+                      f"({tot_t:.1f} s)"}
+
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_09848_b200 as P
+    from paper_2407_09848_b200 import _native as N
+
+    ws, rank, local = dist_env()
+    if ws > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.cuda.current_device()
+    m = args.m
+    c = N.ctx(dev)
+    D = P.poisson3d_device(m)
+    n, nnz = D.nrows, D.nnz
+    M = P.L1JacobiData(m_diag=D.l1_diag())
+    g = torch.Generator(device="cuda").manual_seed(1234 + rank)
+    b = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    x0 = torch.randn(n, dtype=torch.float64, device="cuda", generator=g)
+    cfgs = [P.PolySmootherConfig(family=f, degree=k) for f, k in SWEEP]
+    step_bytes = sum(apply_bytes(n, nnz, k) for _, k in SWEEP)
+
+    def step(evs=None):
+        for i, cfg in enumerate(cfgs):
+            if evs is not None:
+                evs[i][0].record(c.stream)
+            P.smoother_apply(cfg, D, M, b, x0)
+            if evs is not None:
+                evs[i][1].record(c.stream)
+
+    def barrier():
+        if ws > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    sampler = ClockSampler(dev)
+    sampler.start()
+    per = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+            for _ in cfgs] for _ in range(args.steps)]
+    t_start = torch.cuda.Event(enable_timing=True)
+    t_end = torch.cuda.Event(enable_timing=True)
+    launches0 = c.launches()
+    t_start.record(c.stream)
+    for s in range(args.steps):
+        step(per[s])
+    t_end.record(c.stream)
+    torch.cuda.synchronize()
+    launches = c.launches() - launches0
+    clocks = sampler.stop()
+    ms = t_start.elapsed_time(t_end)
+    if ws > 1:
+        t = torch.tensor([ms], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = ws * step_bytes / (ms_step * 1e-3) / 1e9
+
+    # per-(family, degree) apply times -> middle-step kernel time per family
+    t_apply = {}
+    for i, (f, k) in enumerate(SWEEP):
+        t_apply[(f, k)] = statistics.mean(per[s][i][0].elapsed_time(per[s][i][1])
+                                          for s in range(args.steps))
+    mids = {f: (t_apply[(f, 6)] - t_apply[(f, 2)]) / 4.0 for f in ("opt_cheb1", "cheb4", "opt_cheb4")}
+    peak, peak_kind = peaks()
+    mb = mid_step_bytes(n, nnz)
+    t_mid = mids["cheb4"]
+    achieved = mb / (t_mid * 1e-3) / 1e9
+    traffic = traffic_per_launch()
+
+    # end-to-end through the public API from pinned host memory (inputs
+    # uploaded and result downloaded every application)
+    bh = b.cpu().pin_memory()
+    xh = x0.cpu().pin_memory()
+    for cfg in cfgs[:3]:
+        P.smoother_apply(cfg, D, M, bh, xh)
+    barrier()
+    e2e_steps = max(1, min(args.steps, 3))
+    t0 = time.perf_counter()
+    for _ in range(e2e_steps):
+        for cfg in cfgs:
+            out = P.smoother_apply(cfg, D, M, bh, xh)
+    torch.cuda.synchronize()
+    e2e_s = (time.perf_counter() - t0) / e2e_steps
+    if ws > 1:
+        t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e = {"value": ws * step_bytes / e2e_s / 1e9, "unit": "GB/s",
+           "h2d_bytes_per_step": len(cfgs) * 2 * n * 8, "d2h_bytes_per_step": len(cfgs) * n * 8}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"poisson3d 7-pt {m}^3 fine level per GPU, smoother sweep "
+                                   "opt_cheb1/cheb4/opt_cheb4 x k=1..6 (18 applies/step)",
+                       "m": m, "n": n, "nnz": nnz, "bytes_per_step": step_bytes,
+                       "l2": "inputs larger than L2 (A = %.2f GB)" % ((12 * nnz + 4 * n) / 1e9),
+                       "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU"},
+            "hbm_frac": value / ws / peak,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_kind": peak_kind,
+                         "kernel": "k_cheb4_step<false,false,false> (middle degree step)",
+                         "bytes_per_launch": mb, "ms_per_launch": t_mid,
+                         "traffic": (traffic or {}).get("bytes_per_launch")},
+            "mid_step_ms": mids,
+            "apply_ms": {f"{f}_k{k}": v for (f, k), v in t_apply.items()},
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clocks,
+        }
+        if ws == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_baseline(args.cpu_m)
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--m", type=int, default=256)
+    ap.add_argument("--cpu-m", type=int, default=256)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_b200(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

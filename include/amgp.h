@@ -1,0 +1,164 @@
+/*
+ * amgp.h -- C ABI of the B200-native polynomial-smoother / AMG V-cycle / PCG
+ * library (libamgp.so, sm_100a).
+ *
+ * Every entry point replaces one function of the reference package
+ * (/root/reference/pkg/src/amgpoly, cited file:line below) on the hot path
+ * named by BASELINE.json's north_star.  Plain pointers and sizes only:
+ *   - "host" arrays are ordinary CPU memory,
+ *   - "device" arrays are CUDA device pointers on the context's device
+ *     (e.g. torch.Tensor.data_ptr()).
+ * All work is enqueued on the context's stream; functions that return data
+ * to the host synchronise that stream.
+ *
+ * Return value: AMGP_OK (0) or a negative status; amgp_last_error() gives the
+ * thread-local message.  The Python shim maps AMGP_EINVAL to ValueError (the
+ * reference's convention, e.g. sparse.py:121-122, smoothers.py:100-101) and
+ * the others to RuntimeError.
+ */
+#ifndef AMGP_H
+#define AMGP_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define AMGP_OK 0
+#define AMGP_EINVAL (-1) /* dimension mismatch / invalid configuration */
+#define AMGP_ECUDA (-2)  /* CUDA runtime error */
+#define AMGP_ENOMEM (-3) /* device allocation failed */
+#define AMGP_ENCCL (-4)  /* NCCL error */
+
+/* smoothers.py:28 FAMILIES */
+enum { AMGP_L1_JACOBI = 0, AMGP_CHEB4 = 1, AMGP_OPT_CHEB4 = 2, AMGP_OPT_CHEB1 = 3 };
+
+/* krylov.py:15-26 KrylovConfig.variant */
+enum { AMGP_PCG = 0, AMGP_FCG = 1 };
+
+/* amg.py:65 AmgHierarchy.coarse_solver; AMGP_COARSE_SMOOTHER applies the
+ * coarsest level's own smoother from a zero guess, which turns a one-level
+ * hierarchy into smoothers.py:193-199 as_preconditioner. */
+enum { AMGP_COARSE_L1_JACOBI = 0, AMGP_COARSE_DENSE_DIRECT = 1, AMGP_COARSE_SMOOTHER = 2 };
+
+typedef struct amgp_ctx amgp_ctx;   /* device + stream (+ optional NCCL communicator) */
+typedef struct amgp_mat amgp_mat;   /* device matrix in SELL-32 layout */
+typedef struct amgp_hier amgp_hier; /* device AMG hierarchy */
+
+/* smoothers.py:52-85 PolySmootherConfig after __post_init__ resolution. */
+typedef struct {
+    int32_t family;      /* AMGP_* family */
+    int32_t degree;      /* k >= 1 */
+    double a;            /* opt_cheb1 interval end, 0 < a < 1 */
+    double rho_scale;    /* > 0; 1 for l1-Jacobi */
+    const double *beta;  /* host, `degree` entries (opt_cheb4 only; else NULL) */
+} amgp_smoother_cfg;
+
+/* krylov.py:29-38 SolveReport */
+typedef struct {
+    int32_t iterations;
+    int32_t converged;
+    int32_t breakdown;
+    int32_t spmv_count;
+    int32_t precond_count;
+    int32_t n_history;
+    double final_relres;
+    double elapsed_s;
+} amgp_solve_report;
+
+const char *amgp_last_error(void);
+int amgp_version(void);
+
+/* ---- context ----------------------------------------------------------- */
+/* stream: a cudaStream_t (NULL = create a private non-blocking stream). */
+int amgp_ctx_create(int device, void *stream, amgp_ctx **out);
+int amgp_ctx_destroy(amgp_ctx *ctx);
+int amgp_ctx_set_stream(amgp_ctx *ctx, void *stream);
+int amgp_ctx_sync(amgp_ctx *ctx);
+/* number of kernels this context has launched (graph replays count their nodes) */
+int amgp_ctx_launch_count(amgp_ctx *ctx, int64_t *count);
+int amgp_malloc(amgp_ctx *ctx, int64_t bytes, void **dptr);
+int amgp_free(amgp_ctx *ctx, void *dptr);
+int amgp_memcpy_h2d(amgp_ctx *ctx, void *dst_dev, const void *src_host, int64_t bytes);
+int amgp_memcpy_d2h(amgp_ctx *ctx, void *dst_host, const void *src_dev, int64_t bytes);
+
+/* ---- matrices (sparse.py:32-115 CsrMatrix) ----------------------------- */
+/* Upload a host CSR (row_ptr int64[nrows+1], col_idx int64[nnz], values
+ * f64[nnz]; columns sorted per row as CsrMatrix guarantees, sparse.py:43-75)
+ * and pack it into SELL-32.  Per-row entry order is kept, so the device SpMV
+ * accumulates in exactly the reference's order. */
+int amgp_mat_from_csr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *row_ptr,
+                      const int64_t *col_idx, const double *values, amgp_mat **out);
+/* Rows [row_begin, row_end) of the 3D Poisson matrix on an m^3 grid generated
+ * directly on the device (problems.py:32-60 conventions: x-fastest ordering,
+ * Dirichlet rows eliminated, diagonal 6 and -1 per neighbour for stencil 7;
+ * diagonal 26 and -1 per neighbour for stencil 27).  Columns are global. */
+int amgp_mat_poisson3d(amgp_ctx *ctx, int64_t m, int stencil, int64_t row_begin,
+                       int64_t row_end, amgp_mat **out);
+int amgp_mat_destroy(amgp_mat *A);
+/* stored = padded SELL slots; bytes = device bytes of the matrix arrays */
+int amgp_mat_info(const amgp_mat *A, int64_t *nrows, int64_t *ncols, int64_t *nnz,
+                  int64_t *stored, int64_t *bytes);
+/* Download back to host CSR (row_ptr[nrows+1], col_idx[nnz], values[nnz]). */
+int amgp_mat_to_csr(amgp_mat *A, int64_t *row_ptr, int64_t *col_idx, double *values);
+/* smoothers.py:38-49 l1_jacobi_diag: m_i = sum_j |a_ij| - |a_ii| + a_ii,
+ * written to device m[nrows]; AMGP_EINVAL for a non-positive diagonal. */
+int amgp_mat_l1_diag(amgp_mat *A, double *m_dev);
+
+/* ---- hot-path kernels --------------------------------------------------- */
+/* sparse.py:118-125 spmv: y = A x (device vectors). */
+int amgp_spmv(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y);
+/* sparse.py:128-139 fused_update: r -= s; d = d*(rho*rho_prev) + c*r; x += d. */
+int amgp_fused_update(amgp_ctx *ctx, int64_t n, double rho, double rho_prev, double c,
+                      const double *s, double *r, double *d, double *x);
+/* smoothers.py:92-137 smoother_apply: x = S(b, x0), exactly `degree` SpMVs
+ * (logically; the x0 == NULL SpMV of a zero vector is skipped on device).
+ * x0 == NULL means a zero initial guess; x0 may equal x. */
+int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
+                        const amgp_smoother_cfg *cfg, const double *b, const double *x0,
+                        double *x);
+
+/* ---- V-cycle (amg.py:47-91, 293-319) ----------------------------------- */
+/* Levels fine->coarse: A[l], m[l] (device l1 diagonals), P[l] (n_l x n_{l+1})
+ * and R[l] = P[l]^T (amg.py:56-59) for l < nlevels-1.  The hierarchy keeps
+ * references to the matrices and diagonals (caller keeps them alive). */
+int amgp_hier_create(amgp_ctx *ctx, int nlevels, amgp_mat *const *A, const double *const *m,
+                     amgp_mat *const *P, amgp_mat *const *R, int coarse_solver,
+                     int coarse_sweeps, amgp_hier **out);
+/* Smoother of one level (level < 0: all levels), amg.py:51 Level.smoother. */
+int amgp_hier_set_smoother(amgp_hier *h, int level, const amgp_smoother_cfg *cfg);
+/* dense_direct coarse solver: host column-major Cholesky factor L (n x n,
+ * lower) of the coarsest A; solves run on the device (amg.py:295-298). */
+int amgp_hier_set_coarse_cholesky(amgp_hier *h, const double *L_colmajor);
+/* Capture the V-cycle into a CUDA graph on the next apply (1) or not (0). */
+int amgp_hier_use_graph(amgp_hier *h, int enable);
+int amgp_hier_destroy(amgp_hier *h);
+/* amg.py:303-315 vcycle_apply: z = V(r), r and z device vectors of n_0. */
+int amgp_vcycle_apply(amgp_hier *h, const double *r, double *z);
+
+/* ---- Krylov (krylov.py:45-120) ----------------------------------------- */
+/* Solve A x = b with PCG/FCG preconditioned by the V-cycle of h (NULL: none).
+ * x is the initial guess when x0_given, else it is zeroed.  history_host may
+ * be NULL, else it receives up to itmax+1 relative residuals. */
+int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const double *b, double *x,
+                   int x0_given, int variant, double tol, int itmax, double *history_host,
+                   amgp_solve_report *report);
+
+/* ---- host-side helpers (no device needed; used by CPU tests) ------------ */
+/* Pack a CSR into SELL-32 on the host.  Call with outputs NULL to get
+ * *nslices and *stored; then with arrays slice_ptr[nslices+1], col[stored]
+ * (int32, -1 = padding), val[stored]. */
+int amgp_sell_pack_host(int64_t nrows, const int64_t *row_ptr, const int64_t *col_idx,
+                        const double *values, int64_t *nslices, int64_t *stored,
+                        int64_t *slice_ptr, int32_t *col, double *val);
+/* Per-step scalars of smoother_apply computed with the reference's
+ * expressions (smoothers.py:112-135); coef[3*degree]: for cheb4/opt_cheb4
+ * (cz_j, cr_j, beta_j); for opt_cheb1 coef[0]=theta and (rho_j*rho_{j-1},
+ * 2 rho_j/delta) for j=1..degree-1 at coef[1+2(j-1)].  */
+int amgp_smoother_coefficients(const amgp_smoother_cfg *cfg, double *coef);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AMGP_H */

@@ -1,0 +1,183 @@
+// Internal declarations shared by the libamgp.so translation units.
+//
+// Numerics contract: every kernel
+// evaluates the reference's numpy expressions element by element with
+// separate IEEE-754 binary64 operations -- __dmul_rn / __dadd_rn / __dsub_rn /
+// __ddiv_rn, never a contracted FMA (the library is also built with
+// -fmad=false) -- and every sparse row sum starts at 0.0 and accumulates in
+// stored-entry order, exactly like scipy's csr_matvec behind
+// reference sparse.py:125.  One thread owns one row, so the results are
+// bitwise identical to the reference's.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/amgp.h"
+
+#define AMGP_SLICE 32  // SELL slice height == warp width
+
+// ---------------------------------------------------------------- errors
+void amgp_set_error(const std::string &msg);
+int amgp_fail(int code, const std::string &msg);
+int amgp_cuda_fail(cudaError_t e, const char *what, const char *file, int line);
+
+#define AMGP_CUDA(call)                                                        \
+    do {                                                                       \
+        cudaError_t _e = (call);                                               \
+        if (_e != cudaSuccess) return amgp_cuda_fail(_e, #call, __FILE__, __LINE__); \
+    } while (0)
+
+#define AMGP_CHECK_LAUNCH(ctx)                                                 \
+    do {                                                                       \
+        cudaError_t _e = cudaGetLastError();                                   \
+        if (_e != cudaSuccess) return amgp_cuda_fail(_e, "kernel launch", __FILE__, __LINE__); \
+        (ctx)->launches.fetch_add(1, std::memory_order_relaxed);               \
+    } while (0)
+
+#define AMGP_TRY(call)                                                         \
+    do {                                                                       \
+        int _s = (call);                                                       \
+        if (_s != AMGP_OK) return _s;                                          \
+    } while (0)
+
+// ---------------------------------------------------------------- objects
+struct amgp_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    std::atomic<int64_t> launches{0};
+    std::mutex mu;  // serialises API calls that share ctx scratch
+    // deterministic-reduction scratch (PCG): partial sums + scalars
+    double *red_partial = nullptr;
+    int64_t red_partial_n = 0;
+    double *scalars = nullptr;       // device scalar block (see pcg.cu)
+    double *host_scalars = nullptr;  // pinned mirror
+};
+
+struct amgp_mat {
+    amgp_ctx *ctx = nullptr;
+    int64_t nrows = 0, ncols = 0, nnz = 0;
+    int64_t nslices = 0, stored = 0;
+    int64_t *slice_ptr = nullptr;  // [nslices+1] element offsets (multiples of 32)
+    int32_t *col = nullptr;        // [stored], -1 = padding
+    double *val = nullptr;         // [stored]
+    int32_t max_width = 0;
+    int64_t row_offset = 0;  // first global row of a generated row block
+    // per-matrix smoother workspace (r, two operand buffers, x copy)
+    double *work = nullptr;
+    int64_t work_n = 0;
+    std::mutex mu;
+};
+
+// Plain-old-data view passed to kernels.
+struct SellView {
+    const int64_t *__restrict__ slice_ptr;
+    const int32_t *__restrict__ col;
+    const double *__restrict__ val;
+    int64_t nrows;
+    int64_t nslices;
+};
+
+inline SellView view_of(const amgp_mat *A) {
+    return SellView{A->slice_ptr, A->col, A->val, A->nrows, A->nslices};
+}
+
+// Resolved smoother configuration with host-computed step scalars
+// (smoothers.py:112-135 expressions evaluated in binary64 on the host).
+struct SmootherPlan {
+    int family = AMGP_L1_JACOBI;
+    int degree = 1;
+    double rho = 1.0;
+    std::vector<double> coef;  // layout documented at amgp_smoother_coefficients
+};
+
+int make_smoother_plan(const amgp_smoother_cfg *cfg, SmootherPlan *plan);
+
+// Workspace needed by smoother_enqueue for an n-row matrix (doubles).
+inline int64_t smoother_work_doubles(int64_t n) { return 4 * n; }
+
+// Enqueue one smoother application on ctx->stream.  x0 == nullptr: zero
+// initial guess.  x0 must not alias x.  work: smoother_work_doubles(n).
+int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const SmootherPlan &p,
+                     const double *b, const double *x0, double *x, double *work);
+
+// y = A x ; y = r - A x ; x += P xc  (thread per row, stored order)
+int spmv_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y);
+int residual_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *r, const double *x,
+                     double *res);
+int prolong_add_enqueue(amgp_ctx *ctx, const amgp_mat *P, const double *xc, double *x);
+
+// Grid helpers
+inline unsigned grid_for(int64_t nthreads, int block) {
+    return (unsigned)((nthreads + block - 1) / block);
+}
+
+// ---------------------------------------------------------------- device helpers
+// L2 cache policies (createpolicy): matrix slots are streamed once per step
+// (evict_first); gathered operands are reused by neighbouring rows
+// (evict_last).  The per-load .L2::evict_* qualifiers need 256-bit loads on
+// sm_100, so scalar loads carry the policy via .L2::cache_hint.
+__device__ __forceinline__ uint64_t policy_evict_first() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+    uint64_t p;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+    return p;
+}
+__device__ __forceinline__ double ld_stream_f64(const double *p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.f64 %0, [%1], %2;"
+                 : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ int32_t ld_stream_s32(const int32_t *p, uint64_t pol) {
+    int32_t v;
+    asm("ld.global.nc.L1::no_allocate.L2::cache_hint.s32 %0, [%1], %2;"
+                 : "=r"(v) : "l"(p), "l"(pol));
+    return v;
+}
+__device__ __forceinline__ double ld_gather_f64(const double *p, uint64_t pol) {
+    double v;
+    asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+    return v;
+}
+
+// Row sum of slice row `lane` of slice `s`: sum_j val*x[col] from 0.0 in slot
+// order (== CSR stored order).  Slots are loaded U at a time (predicated) so
+// a warp keeps 2U streaming loads + U gathers in flight.  Padding slots
+// (col < 0) contribute nothing.
+template <int U>
+__device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int lane,
+                                               const double *__restrict__ x) {
+    const int64_t base = A.slice_ptr[s];
+    const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
+    const int32_t *c = A.col + base + lane;
+    const double *v = A.val + base + lane;
+    const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+    double sum = 0.0;
+    for (int j = 0; j < w; j += U) {
+        int32_t cc[U];
+        double vv[U], xx[U];
+#pragma unroll
+        for (int u = 0; u < U; u++) {
+            const bool ok = j + u < w;
+            cc[u] = ok ? ld_stream_s32(c + (int64_t)(j + u) * AMGP_SLICE, pf) : -1;
+            vv[u] = ok ? ld_stream_f64(v + (int64_t)(j + u) * AMGP_SLICE, pf) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < U; u++) xx[u] = cc[u] >= 0 ? ld_gather_f64(x + cc[u], pl) : 0.0;
+#pragma unroll
+        for (int u = 0; u < U; u++)
+            if (cc[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(vv[u], xx[u]));
+    }
+    return sum;
+}

@@ -1,0 +1,330 @@
+// K7: PCG / FCG on the device (reference krylov.py:45-120).
+//
+// Every PCG scalar stays on the device; the host only reads back the relative
+// residual (and the breakdown flag) once per iteration to decide termination.
+// Dots are deterministic: a fixed grid, per-thread sequential partials,
+// xor-butterfly warp sums, a fixed block tree, and the last block to finish
+// (atomic ticket) folds the per-block partials in block order -- the same
+// bits on every run.  Their order differs from OpenBLAS ddot, hence the
+// reference's +-1 iteration tolerance.
+//
+// One iteration (fusions in brackets):
+//   [Ad = A d ; d.Ad (; r.d)] -> dAd, alpha, breakdown          k_pcg_spmv_dot
+//   [x += alpha d ; r -= alpha Ad ; r.r] -> relres              k_pcg_update
+//   z = V(r)                                                    V-cycle graph
+//   [r.z | z.Ad] -> beta                                        k_pcg_dot
+//   d = z +- beta d                                             k_pcg_dir
+// The host checks relres while the GPU already runs the (harmless when the
+// iteration turns out to be the last) V-cycle and direction update.
+#include <math.h>
+#include <time.h>
+
+#include <algorithm>
+#include <chrono>
+
+#include "amgp_common.cuh"
+
+int vcycle_enqueue(amgp_hier *h, const double *r, double *z);
+int64_t hier_rows(const amgp_hier *h);
+std::mutex &hier_mutex(amgp_hier *h);
+
+enum {
+    S_BNORM = 0, S_RZ, S_DAD, S_ALPHA, S_BETA, S_RELRES, S_BRK, S_RR, S_BB, S_AUX,
+    S_COUNT
+};
+
+#define RB 256          // reduction block
+#define RGRID_MAX 1184  // 148 SMs x 8
+
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double ws[RB / 32];
+    for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __syncthreads();
+    if (lane == 0) ws[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        v = lane < (int)(blockDim.x >> 5) ? ws[lane] : 0.0;
+        for (int o = 16; o > 0; o >>= 1) v = __dadd_rn(v, __shfl_xor_sync(0xffffffffu, v, o));
+    }
+    return v;  // valid in warp 0
+}
+
+// Publish this block's partial(s); returns true in the last block, whose
+// thread 0 then holds the folded totals in tot[0..NV-1].
+template <int NV>
+__device__ bool reduce_partials(const double (&acc)[NV], double *partial, unsigned *ticket,
+                                double (&tot)[NV]) {
+    __shared__ bool last;
+    double bs[NV];
+#pragma unroll
+    for (int q = 0; q < NV; q++) bs[q] = block_sum(acc[q]);
+    if (threadIdx.x == 0) {
+#pragma unroll
+        for (int q = 0; q < NV; q++) partial[q * RGRID_MAX + blockIdx.x] = bs[q];
+        __threadfence();
+        last = atomicAdd(ticket, 1u) == gridDim.x - 1;
+    }
+    __syncthreads();
+    if (!last) return false;
+    __threadfence();
+#pragma unroll
+    for (int q = 0; q < NV; q++) {
+        double t = 0.0;
+        for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x)
+            t = __dadd_rn(t, __ldcg(partial + q * RGRID_MAX + i));
+        tot[q] = block_sum(t);
+    }
+    if (threadIdx.x == 0) *ticket = 0;
+    return threadIdx.x == 0;
+}
+
+// MODE 0: S_BB = b.b -> bnorm ; MODE 1: r.r -> relres ; MODE 2: r.z -> rz (init)
+template <int MODE>
+__global__ void __launch_bounds__(RB)
+k_pcg_dot_init(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
+               double *partial, unsigned *ticket, double *sc) {
+    double acc[1] = {0.0};
+    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(a[i], b[i]));
+    double tot[1];
+    if (reduce_partials<1>(acc, partial, ticket, tot)) {
+        if (MODE == 0) sc[S_BNORM] = sqrt(tot[0]);
+        else if (MODE == 1) sc[S_RELRES] = __ddiv_rn(sqrt(tot[0]), sc[S_BNORM]);
+        else sc[S_RZ] = tot[0];
+        sc[S_BRK] = 0.0;
+    }
+}
+
+template <bool FCG>
+__global__ void __launch_bounds__(RB)
+k_pcg_spmv_dot(SellView A, const double *__restrict__ d, double *__restrict__ Ad,
+               const double *__restrict__ r, double *partial, unsigned *ticket, double *sc) {
+    double acc[2] = {0.0, 0.0};
+    const int lane = threadIdx.x & 31;
+    for (int64_t s = (int64_t)blockIdx.x * (RB / 32) + (threadIdx.x >> 5); s < A.nslices;
+         s += (int64_t)gridDim.x * (RB / 32)) {
+        const double y = sell_row_dot<8>(A, s, lane, d);
+        const int64_t row = s * 32 + lane;
+        if (row < A.nrows) {
+            Ad[row] = y;
+            const double di = d[row];
+            acc[0] = __dadd_rn(acc[0], __dmul_rn(di, y));
+            if (FCG) acc[1] = __dadd_rn(acc[1], __dmul_rn(r[row], di));
+        }
+    }
+    double tot[2];
+    if (reduce_partials<2>(acc, partial, ticket, tot)) {
+        const double dAd = tot[0];
+        sc[S_DAD] = dAd;
+        if (dAd <= 0.0) sc[S_BRK] = 1.0;                      // krylov.py:97-99
+        sc[S_ALPHA] = FCG ? __ddiv_rn(tot[1], dAd) : __ddiv_rn(sc[S_RZ], dAd);  // :100
+    }
+}
+
+__global__ void __launch_bounds__(RB)
+k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
+             const double *__restrict__ d, const double *__restrict__ Ad, double *partial,
+             unsigned *ticket, double *sc) {
+    if (sc[S_BRK] != 0.0) return;  // breakdown: x, r stay as the reference returns them
+    const double alpha = sc[S_ALPHA];
+    double acc[1] = {0.0};
+    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, d[i]));   // krylov.py:101
+        const double ri = __dsub_rn(r[i], __dmul_rn(alpha, Ad[i]));  // :102
+        r[i] = ri;
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(ri, ri));
+    }
+    double tot[1];
+    if (reduce_partials<1>(acc, partial, ticket, tot))
+        sc[S_RELRES] = __ddiv_rn(sqrt(tot[0]), sc[S_BNORM]);  // :103
+}
+
+template <bool FCG>
+__global__ void __launch_bounds__(RB)
+k_pcg_dot(int64_t n, const double *__restrict__ r, const double *__restrict__ z,
+          const double *__restrict__ Ad, double *partial, unsigned *ticket, double *sc) {
+    if (sc[S_BRK] != 0.0) return;
+    double acc[1] = {0.0};
+    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
+        acc[0] = FCG ? __dadd_rn(acc[0], __dmul_rn(z[i], Ad[i]))
+                     : __dadd_rn(acc[0], __dmul_rn(r[i], z[i]));
+    double tot[1];
+    if (reduce_partials<1>(acc, partial, ticket, tot)) {
+        if (FCG) {
+            sc[S_BETA] = __ddiv_rn(tot[0], sc[S_DAD]);  // krylov.py:118
+        } else {
+            sc[S_BETA] = __ddiv_rn(tot[0], sc[S_RZ]);   // :111-113
+            sc[S_RZ] = tot[0];
+        }
+    }
+}
+
+template <bool FCG>
+__global__ void k_pcg_dir(int64_t n, const double *__restrict__ z, double *__restrict__ d,
+                          const double *sc) {
+    if (sc[S_BRK] != 0.0) return;
+    const double beta = sc[S_BETA];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double bd = __dmul_rn(beta, d[i]);
+        d[i] = FCG ? __dsub_rn(z[i], bd) : __dadd_rn(z[i], bd);  // :114 / :119
+    }
+}
+
+__global__ void k_scale_zero(int64_t n, double *x) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        x[i] = __dmul_rn(x[i], 0.0);
+}
+
+namespace {
+struct PcgWork {
+    double *partial = nullptr;
+    unsigned *ticket = nullptr;
+    double *r = nullptr, *z = nullptr, *d = nullptr, *Ad = nullptr;
+    ~PcgWork() {
+        cudaFree(partial);
+        cudaFree(ticket);
+        cudaFree(r);
+        cudaFree(z);
+        cudaFree(d);
+        cudaFree(Ad);
+    }
+};
+}  // namespace
+
+static unsigned rgrid(int64_t n) {
+    return (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(n, RB), RGRID_MAX));
+}
+
+extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const double *b,
+                              double *x, int x0_given, int variant, double tol, int itmax,
+                              double *history, amgp_solve_report *rep) {
+    if (!ctx || !A || !rep) return amgp_fail(AMGP_EINVAL, "amgp_pcg_solve: bad argument");
+    if (variant != AMGP_PCG && variant != AMGP_FCG)
+        return amgp_fail(AMGP_EINVAL, "unknown Krylov variant");
+    if (!(tol > 0.0) || itmax < 1) return amgp_fail(AMGP_EINVAL, "tol must be positive and itmax >= 1");
+    if (A->nrows != A->ncols) return amgp_fail(AMGP_EINVAL, "matrix must be square");
+    if (h && hier_rows(h) != A->nrows) return amgp_fail(AMGP_EINVAL, "dimension mismatch");
+    const int64_t n = A->nrows;
+    if (n > 0 && (!b || !x)) return amgp_fail(AMGP_EINVAL, "null vector");
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> cg(ctx->mu);
+    auto t0 = std::chrono::steady_clock::now();
+    auto elapsed = [&] {
+        return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    const bool fcg = variant == AMGP_FCG;
+    cudaStream_t st = ctx->stream;
+    double *sc = ctx->scalars, *hs = ctx->host_scalars;
+
+    PcgWork w;
+    const size_t nb = (size_t)std::max<int64_t>(n, 1) * sizeof(double);
+    AMGP_CUDA(cudaMalloc(&w.partial, 2 * RGRID_MAX * sizeof(double)));
+    AMGP_CUDA(cudaMalloc(&w.ticket, 4 * sizeof(unsigned)));
+    AMGP_CUDA(cudaMalloc(&w.r, nb));
+    AMGP_CUDA(cudaMalloc(&w.z, nb));
+    AMGP_CUDA(cudaMalloc(&w.d, nb));
+    AMGP_CUDA(cudaMalloc(&w.Ad, nb));
+    AMGP_CUDA(cudaMemsetAsync(w.ticket, 0, 4 * sizeof(unsigned), st));
+    const unsigned g = rgrid(n);
+    const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(A->nslices, RB / 32), RGRID_MAX));
+
+    *rep = amgp_solve_report{};
+    int nh = 0;
+    auto fetch = [&]() -> int {
+        AMGP_CUDA(cudaMemcpyAsync(hs, sc, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
+        AMGP_CUDA(cudaStreamSynchronize(st));
+        return AMGP_OK;
+    };
+
+    if (!x0_given) AMGP_CUDA(cudaMemsetAsync(x, 0, nb, st));
+    k_pcg_dot_init<0><<<g, RB, 0, st>>>(n, b, b, w.partial, w.ticket, sc);  // bnorm
+    AMGP_CHECK_LAUNCH(ctx);
+    AMGP_TRY(fetch());
+    if (hs[S_BNORM] == 0.0) {  // krylov.py:68-69
+        k_scale_zero<<<g, RB, 0, st>>>(n, x);
+        AMGP_CHECK_LAUNCH(ctx);
+        AMGP_CUDA(cudaStreamSynchronize(st));
+        rep->converged = 1;
+        rep->elapsed_s = elapsed();
+        return AMGP_OK;
+    }
+    AMGP_TRY(residual_enqueue(ctx, A, b, x, w.r));  // r = b - A x (:71)
+    int spmv = 1, pc = 0;
+    k_pcg_dot_init<1><<<g, RB, 0, st>>>(n, w.r, w.r, w.partial, w.ticket, sc);
+    AMGP_CHECK_LAUNCH(ctx);
+    AMGP_TRY(fetch());
+    double relres = hs[S_RELRES];
+    if (history) history[nh] = relres;
+    nh++;
+    auto finish = [&](int it, bool conv, bool brk) {
+        rep->iterations = it;
+        rep->converged = conv;
+        rep->breakdown = brk;
+        rep->final_relres = relres;
+        rep->spmv_count = spmv;
+        rep->precond_count = pc;
+        rep->n_history = nh;
+        rep->elapsed_s = elapsed();
+        return AMGP_OK;
+    };
+    if (relres <= tol) return finish(0, true, false);
+
+    std::unique_lock<std::mutex> hl;
+    if (h) hl = std::unique_lock<std::mutex>(hier_mutex(h));
+    auto precond = [&]() -> int {
+        if (h) return vcycle_enqueue(h, w.r, w.z);
+        AMGP_CUDA(cudaMemcpyAsync(w.z, w.r, nb, cudaMemcpyDeviceToDevice, st));
+        return AMGP_OK;
+    };
+    AMGP_TRY(precond());
+    pc++;
+    AMGP_CUDA(cudaMemcpyAsync(w.d, w.z, nb, cudaMemcpyDeviceToDevice, st));
+    k_pcg_dot_init<2><<<g, RB, 0, st>>>(n, w.r, w.z, w.partial, w.ticket, sc);  // rz
+    AMGP_CHECK_LAUNCH(ctx);
+
+    for (int it = 1; it <= itmax; it++) {
+        if (fcg) k_pcg_spmv_dot<true><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
+        else k_pcg_spmv_dot<false><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
+        AMGP_CHECK_LAUNCH(ctx);
+        spmv++;
+        k_pcg_update<<<g, RB, 0, st>>>(n, x, w.r, w.d, w.Ad, w.partial, w.ticket, sc);
+        AMGP_CHECK_LAUNCH(ctx);
+        AMGP_CUDA(cudaMemcpyAsync(hs, sc, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
+        cudaEvent_t ev;
+        AMGP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        cudaEventRecord(ev, st);
+        // speculative: next preconditioner application and direction update
+        int s1 = precond();
+        if (s1 == AMGP_OK) {
+            if (fcg) k_pcg_dot<true><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
+            else k_pcg_dot<false><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
+            cudaError_t e1 = cudaGetLastError();
+            if (fcg) k_pcg_dir<true><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
+            else k_pcg_dir<false><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
+            cudaError_t e2 = cudaGetLastError();
+            if (e1 != cudaSuccess || e2 != cudaSuccess) s1 = amgp_cuda_fail(e1 != cudaSuccess ? e1 : e2, "pcg kernels", __FILE__, __LINE__);
+            ctx->launches.fetch_add(2);
+        }
+        cudaError_t es = cudaEventSynchronize(ev);
+        cudaEventDestroy(ev);
+        if (s1 != AMGP_OK) return s1;
+        if (es != cudaSuccess) return amgp_cuda_fail(es, "pcg sync", __FILE__, __LINE__);
+        if (hs[S_BRK] != 0.0) {
+            AMGP_CUDA(cudaStreamSynchronize(st));
+            return finish(it - 1, false, true);
+        }
+        relres = hs[S_RELRES];
+        if (history) history[nh] = relres;
+        nh++;
+        if (relres <= tol) {
+            AMGP_CUDA(cudaStreamSynchronize(st));
+            return finish(it, true, false);
+        }
+        pc++;
+    }
+    AMGP_CUDA(cudaStreamSynchronize(st));
+    return finish(itmax, false, false);
+}

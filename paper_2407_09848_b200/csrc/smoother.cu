@@ -1,0 +1,296 @@
+// K1/K2: the fused polynomial-smoother step kernels and smoother_apply.
+//
+// One kernel launch per degree step.  Each launch streams the matrix once
+// (SELL-32, thread per row) and fuses the SpMV of the step's operand with the
+// l1 scaling and the recurrence update of r / z|d / x -- the reference's k
+// SpMVs plus 2-4 numpy passes per step (smoothers.py:106-137) become k
+// passes over HBM.  The operand is double-buffered: rows gather the previous
+// step's operand while the new one is written to the other buffer.
+//
+// Per-element arithmetic, every operation a
+// separate round-to-nearest binary64 op in the reference's order:
+//   l1_jacobi  sweep     : y=A x ; x' = x + ((b - y)/m)                 (:106-110)
+//   cheb4/opt  step 1    : y=A x0; r=b-y ; z=(0*cz)+cr*(r/m); x=x0+beta z (:112-118)
+//              step j>1  : y=A z ; r=r-y ; z=z*cz + cr*(r/m) ; x=x+beta z (:117-122)
+//   opt_cheb1  init      : y=A x0; r=((b-y)/m)/rho ; d=r/theta ; x=x0+d    (:128-131)
+//              step j    : y=A d ; s=(y/m)/rho ; r=r-s ; d=d*rp + c*r ; x=x+d (:132-136)
+// With x0 == 0 the first SpMV is skipped (b - A*0 == b bitwise).
+#include <algorithm>
+
+#include "amgp_common.cuh"
+
+#define SM_BLOCK 256
+#define SM_SLICES (SM_BLOCK / 32)
+#define SM_U 8
+
+// ---------------------------------------------------------------- kernels
+template <bool FIRST, bool LAST, bool X0>
+__global__ void __launch_bounds__(SM_BLOCK)
+k_cheb4_step(SellView A, const double *__restrict__ m, const double *__restrict__ b,
+             const double *__restrict__ xg, double *__restrict__ r, double *__restrict__ znew,
+             double *__restrict__ x, double cz, double cr, double beta) {
+    const int64_t s = (int64_t)blockIdx.x * SM_SLICES + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= A.nslices) return;
+    double y = 0.0;
+    if (!FIRST || X0) y = sell_row_dot<SM_U>(A, s, lane, xg);
+    const int64_t row = s * 32 + lane;
+    if (row >= A.nrows) return;
+    const double rr = __dsub_rn(FIRST ? b[row] : r[row], y);
+    double z = FIRST ? __dmul_rn(0.0, cz) : __dmul_rn(xg[row], cz);
+    z = __dadd_rn(z, __dmul_rn(cr, __ddiv_rn(rr, m[row])));
+    const double xo = FIRST ? (X0 ? xg[row] : 0.0) : x[row];
+    x[row] = __dadd_rn(xo, __dmul_rn(beta, z));
+    if (!LAST) {
+        r[row] = rr;
+        znew[row] = z;
+    }
+}
+
+template <bool FIRST, bool LAST, bool X0, bool RHO1>
+__global__ void __launch_bounds__(SM_BLOCK)
+k_cheb1_step(SellView A, const double *__restrict__ m, const double *__restrict__ b,
+             const double *__restrict__ xg, double *__restrict__ r, double *__restrict__ dnew,
+             double *__restrict__ x, double c0, double c1, double rho) {
+    // FIRST: c0 = theta ; else c0 = rho_j*rho_{j-1}, c1 = 2 rho_j / delta
+    const int64_t s = (int64_t)blockIdx.x * SM_SLICES + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= A.nslices) return;
+    double y = 0.0;
+    if (!FIRST || X0) y = sell_row_dot<SM_U>(A, s, lane, xg);
+    const int64_t row = s * 32 + lane;
+    if (row >= A.nrows) return;
+    double rr, d, xo;
+    if (FIRST) {
+        rr = __ddiv_rn(__dsub_rn(b[row], y), m[row]);
+        if (!RHO1) rr = __ddiv_rn(rr, rho);
+        d = __ddiv_rn(rr, c0);
+        xo = X0 ? xg[row] : 0.0;
+    } else {
+        double sv = __ddiv_rn(y, m[row]);
+        if (!RHO1) sv = __ddiv_rn(sv, rho);
+        rr = __dsub_rn(r[row], sv);
+        d = __dadd_rn(__dmul_rn(xg[row], c0), __dmul_rn(c1, rr));
+        xo = x[row];
+    }
+    x[row] = __dadd_rn(xo, d);
+    if (!LAST) {
+        r[row] = rr;
+        dnew[row] = d;
+    }
+}
+
+template <bool X0>
+__global__ void __launch_bounds__(SM_BLOCK)
+k_l1_sweep(SellView A, const double *__restrict__ m, const double *__restrict__ b,
+           const double *__restrict__ xin, double *__restrict__ xout) {
+    const int64_t s = (int64_t)blockIdx.x * SM_SLICES + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= A.nslices) return;
+    double y = 0.0;
+    if (X0) y = sell_row_dot<SM_U>(A, s, lane, xin);
+    const int64_t row = s * 32 + lane;
+    if (row >= A.nrows) return;
+    const double rr = __dsub_rn(b[row], y);
+    xout[row] = __dadd_rn(X0 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
+}
+
+// sparse.py:128-139 fused_update (elementwise, in place)
+__global__ void k_fused_update(int64_t n, double rp, double c, const double *__restrict__ s,
+                               double *__restrict__ r, double *__restrict__ d,
+                               double *__restrict__ x) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double ri = __dsub_rn(r[i], s[i]);
+        const double di = __dadd_rn(__dmul_rn(d[i], rp), __dmul_rn(c, ri));
+        r[i] = ri;
+        d[i] = di;
+        x[i] = __dadd_rn(x[i], di);
+    }
+}
+
+// ---------------------------------------------------------------- host side
+// smoothers.py:112-135 scalars, evaluated as Python evaluates them (binary64,
+// left-to-right; host code is compiled with -ffp-contract=off semantics since
+// every operation is a separate statement on doubles).
+int make_smoother_plan(const amgp_smoother_cfg *cfg, SmootherPlan *plan) {
+    if (!cfg) return amgp_fail(AMGP_EINVAL, "null smoother config");
+    if (cfg->family < AMGP_L1_JACOBI || cfg->family > AMGP_OPT_CHEB1)
+        return amgp_fail(AMGP_EINVAL, "unknown smoother family");
+    if (cfg->degree < 1) return amgp_fail(AMGP_EINVAL, "degree must be >= 1");
+    if (!(cfg->rho_scale > 0.0)) return amgp_fail(AMGP_EINVAL, "rho_scale must be positive");
+    const int k = cfg->degree;
+    plan->family = cfg->family;
+    plan->degree = k;
+    plan->rho = cfg->rho_scale;
+    plan->coef.assign(3 * (size_t)k, 0.0);
+    const double rho = cfg->rho_scale;
+    if (cfg->family == AMGP_CHEB4 || cfg->family == AMGP_OPT_CHEB4) {
+        if (cfg->family == AMGP_OPT_CHEB4 && !cfg->beta)
+            return amgp_fail(AMGP_EINVAL, "opt_cheb4 needs a beta table");
+        for (int j = 1; j <= k; j++) {
+            double num = (double)(8 * j - 4), den = (double)(2 * j + 1);
+            double q = num / den;
+            double cr = q / rho;
+            double cz = (double)(2 * j - 3) / den;
+            plan->coef[3 * (j - 1) + 0] = cz;
+            plan->coef[3 * (j - 1) + 1] = cr;
+            plan->coef[3 * (j - 1) + 2] = cfg->family == AMGP_OPT_CHEB4 ? cfg->beta[j - 1] : 1.0;
+        }
+    } else if (cfg->family == AMGP_OPT_CHEB1) {
+        if (!(cfg->a > 0.0 && cfg->a < 1.0)) return amgp_fail(AMGP_EINVAL, "a must lie in (0, 1)");
+        // chebyshev.py:82-83
+        double theta = (1.0 + cfg->a) / 2.0;
+        double delta = (1.0 - cfg->a) / 2.0;
+        double sigma1 = theta / delta;
+        plan->coef[0] = theta;
+        double rho_prev = 1.0 / sigma1;
+        for (int j = 1; j < k; j++) {
+            double t = 2.0 * sigma1;
+            double rho_cur = 1.0 / (t - rho_prev);
+            double rp = rho_cur * rho_prev;
+            double c2 = 2.0 * rho_cur;
+            double c = c2 / delta;
+            plan->coef[1 + 2 * (j - 1)] = rp;
+            plan->coef[2 + 2 * (j - 1)] = c;
+            rho_prev = rho_cur;
+        }
+    }
+    return AMGP_OK;
+}
+
+extern "C" int amgp_smoother_coefficients(const amgp_smoother_cfg *cfg, double *coef) {
+    SmootherPlan p;
+    AMGP_TRY(make_smoother_plan(cfg, &p));
+    if (coef) std::copy(p.coef.begin(), p.coef.end(), coef);
+    return AMGP_OK;
+}
+
+template <bool FIRST, bool LAST>
+static void launch_cheb4(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
+                         const double *xg, bool x0, double *r, double *znew, double *x,
+                         double cz, double cr, double beta) {
+    const unsigned g = grid_for(A->nslices, SM_SLICES);
+    if (FIRST && x0)
+        k_cheb4_step<FIRST, LAST, true><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, znew, x, cz, cr, beta);
+    else
+        k_cheb4_step<FIRST, LAST, false><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, znew, x, cz, cr, beta);
+}
+
+template <bool FIRST, bool LAST, bool X0>
+static void launch_cheb1_x0(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
+                            const double *xg, double *r, double *dnew, double *x, double c0,
+                            double c1, double rho) {
+    const unsigned g = grid_for(A->nslices, SM_SLICES);
+    if (rho == 1.0)
+        k_cheb1_step<FIRST, LAST, X0, true><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, dnew, x, c0, c1, rho);
+    else
+        k_cheb1_step<FIRST, LAST, X0, false><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, dnew, x, c0, c1, rho);
+}
+
+template <bool FIRST, bool LAST>
+static void launch_cheb1(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
+                         const double *xg, bool x0, double *r, double *dnew, double *x,
+                         double c0, double c1, double rho) {
+    if (FIRST && x0) launch_cheb1_x0<FIRST, LAST, true>(ctx, A, m, b, xg, r, dnew, x, c0, c1, rho);
+    else launch_cheb1_x0<FIRST, LAST, false>(ctx, A, m, b, xg, r, dnew, x, c0, c1, rho);
+}
+
+int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const SmootherPlan &p,
+                     const double *b, const double *x0, double *x, double *work) {
+    const int64_t n = A->nrows;
+    if (n == 0) return AMGP_OK;
+    const int k = p.degree;
+    double *r = work, *buf[2] = {work + 2 * n, work + n}, *tmp = work + 3 * n;
+    const bool hx0 = x0 != nullptr;
+    if (p.family == AMGP_L1_JACOBI) {
+        // sweep s writes x when (k - s) is even, else tmp, so sweep k lands in x
+        const double *xin = x0;
+        for (int s = 1; s <= k; s++) {
+            double *xout = ((k - s) % 2 == 0) ? x : tmp;
+            const unsigned g = grid_for(A->nslices, SM_SLICES);
+            if (s == 1 && !hx0)
+                k_l1_sweep<false><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, nullptr, xout);
+            else
+                k_l1_sweep<true><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xin, xout);
+            AMGP_CHECK_LAUNCH(ctx);
+            xin = xout;
+        }
+        return AMGP_OK;
+    }
+    if (p.family == AMGP_CHEB4 || p.family == AMGP_OPT_CHEB4) {
+        for (int j = 1; j <= k; j++) {
+            const double cz = p.coef[3 * (j - 1)], cr = p.coef[3 * (j - 1) + 1],
+                         be = p.coef[3 * (j - 1) + 2];
+            const double *xg = (j == 1) ? x0 : buf[(j - 1) & 1];
+            double *zn = buf[j & 1];
+            if (j == 1 && k == 1) launch_cheb4<true, true>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
+            else if (j == 1) launch_cheb4<true, false>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
+            else if (j == k) launch_cheb4<false, true>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
+            else launch_cheb4<false, false>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
+            AMGP_CHECK_LAUNCH(ctx);
+        }
+        return AMGP_OK;
+    }
+    // opt_cheb1: launch 0 is the init, launches j = 1..k-1 the fused updates
+    for (int j = 0; j < k; j++) {
+        const double *xg = (j == 0) ? x0 : buf[j & 1];
+        double *dn = buf[(j + 1) & 1];
+        const bool last = (j == k - 1);
+        if (j == 0) {
+            const double theta = p.coef[0];
+            if (last) launch_cheb1<true, true>(ctx, A, m, b, xg, hx0, r, dn, x, theta, 0.0, p.rho);
+            else launch_cheb1<true, false>(ctx, A, m, b, xg, hx0, r, dn, x, theta, 0.0, p.rho);
+        } else {
+            const double rp = p.coef[1 + 2 * (j - 1)], c = p.coef[2 + 2 * (j - 1)];
+            if (last) launch_cheb1<false, true>(ctx, A, m, b, xg, hx0, r, dn, x, rp, c, p.rho);
+            else launch_cheb1<false, false>(ctx, A, m, b, xg, hx0, r, dn, x, rp, c, p.rho);
+        }
+        AMGP_CHECK_LAUNCH(ctx);
+    }
+    return AMGP_OK;
+}
+
+static int ensure_work(amgp_mat *A, int64_t doubles) {
+    if (A->work_n >= doubles) return AMGP_OK;
+    cudaStreamSynchronize(A->ctx->stream);
+    cudaFree(A->work);
+    A->work = nullptr;
+    A->work_n = 0;
+    AMGP_CUDA(cudaMalloc(&A->work, (size_t)doubles * sizeof(double)));
+    A->work_n = doubles;
+    return AMGP_OK;
+}
+
+extern "C" int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
+                                   const amgp_smoother_cfg *cfg, const double *b,
+                                   const double *x0, double *x) {
+    if (!ctx || !A || !cfg) return amgp_fail(AMGP_EINVAL, "amgp_smoother_apply: bad argument");
+    if (A->nrows != A->ncols) return amgp_fail(AMGP_EINVAL, "dimension mismatch");
+    if (A->nrows > 0 && (!m || !b || !x)) return amgp_fail(AMGP_EINVAL, "null vector");
+    SmootherPlan p;
+    AMGP_TRY(make_smoother_plan(cfg, &p));
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> g(A->mu);
+    const int64_t n = A->nrows;
+    AMGP_TRY(ensure_work(A, smoother_work_doubles(n) + n));
+    if (x0 && x0 == x) {  // x0 may alias x: keep a private copy of x0
+        double *x0c = A->work + smoother_work_doubles(n);
+        AMGP_CUDA(cudaMemcpyAsync(x0c, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        x0 = x0c;
+    }
+    return smoother_enqueue(ctx, A, m, p, b, x0, x, A->work);
+}
+
+extern "C" int amgp_fused_update(amgp_ctx *ctx, int64_t n, double rho, double rho_prev, double c,
+                                 const double *s, double *r, double *d, double *x) {
+    if (!ctx || n < 0) return amgp_fail(AMGP_EINVAL, "fused_update: vector length mismatch");
+    if (n == 0) return AMGP_OK;
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    const double rp = rho * rho_prev;  // sparse.py:137 evaluates rho*rho_prev first
+    const int blk = 256;
+    const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, blk), 148 * 16);
+    k_fused_update<<<g, blk, 0, ctx->stream>>>(n, rp, c, s, r, d, x);
+    AMGP_CHECK_LAUNCH(ctx);
+    return AMGP_OK;
+}

@@ -1,0 +1,343 @@
+"""GPU parity: the CUDA path through the C ABI against the reference.
+
+Bar (BASELINE.json north_star): smoother output within 1e-12 relative in
+fp64; these kernels reproduce the reference bitwise, so every comparison
+here is np.array_equal unless stated.  References: the reference's own
+outputs (tests/golden/*.npz, made by importing the reference) and the C
+oracle (oracle/, pinned to those goldens by tests/test_oracle.py) for sizes
+beyond the fixtures.
+"""
+
+import numpy as np
+import pytest
+
+import oracle
+from conftest import golden, golden_levels, golden_mat, gpu_available, smoother_params
+
+pytestmark = pytest.mark.gpu
+
+FAMILIES = ("l1_jacobi", "cheb4", "opt_cheb4", "opt_cheb1")
+SMALL = ("tridiag20", "p3d6", "p3d8", "spd30")
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not gpu_available():
+        pytest.skip("no CUDA device")
+    import paper_2407_09848_b200 as pkg
+
+    return pkg
+
+
+def small_csr(P, name):
+    d = golden("smoother_small.npz")
+    return P.CsrMatrix(*golden_mat(d, name)), d
+
+
+def test_native_library_is_loaded(P):
+    from paper_2407_09848_b200 import _native as N
+
+    c = N.ctx()
+    before = c.launches()
+    A, _ = small_csr(P, "p3d6")
+    P.spmv(A, np.ones(A.ncols))
+    assert c.launches() > before
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_spmv_bitwise(P, name):
+    A, d = small_csr(P, name)
+    x = d[name + "_x0"]
+    want = oracle.spmv(A.row_ptr, A.col_idx, A.values, A.ncols, x)
+    assert np.array_equal(P.spmv(A, x), want)
+    assert np.array_equal(P.spmv(A, A.to_dense()[:, 1] * 0 + 1.0),
+                          oracle.spmv(A.row_ptr, A.col_idx, A.values, A.ncols, np.ones(A.ncols)))
+
+
+def test_spmv_exact_cases(P):
+    eye = P.CsrMatrix.identity(3)
+    x = np.array([1.0, 2.0, 3.0])
+    assert np.array_equal(P.spmv(eye, x), x)
+    with pytest.raises(ValueError):
+        P.spmv(eye, np.ones(4))
+    A, _ = P.poisson3d(2)
+    e1 = np.zeros(8)
+    e1[1] = 1.0
+    assert np.array_equal(P.spmv(A, e1), A.to_dense()[:, 1])
+
+
+@pytest.mark.parametrize("name", SMALL)
+@pytest.mark.parametrize("fam", FAMILIES)
+def test_smoother_apply_bitwise_vs_reference(P, name, fam):
+    A, d = small_csr(P, name)
+    M = P.L1JacobiData(m_diag=d[name + "_m"])
+    b, x0 = d[name + "_b"], d[name + "_x0"]
+    for k in range(1, 9):
+        cfg = P.PolySmootherConfig(family=fam, degree=k)
+        got = P.smoother_apply(cfg, A, M, b, x0)
+        assert np.array_equal(got, d[f"{name}_{fam}_k{k}_x0"]), (fam, k)
+        got = P.smoother_apply(cfg, A, M, b, np.zeros_like(b))
+        assert np.array_equal(got, d[f"{name}_{fam}_k{k}_zero"]), (fam, k)
+    cfg = P.PolySmootherConfig(family=fam, degree=3, rho_scale=1.3)
+    assert np.array_equal(P.smoother_apply(cfg, A, M, b, x0), d[f"{name}_{fam}_rho1.3_k3_x0"])
+
+
+def test_smoother_closed_forms(P):
+    d = golden("smoother_small.npz")
+    A = P.CsrMatrix(*golden_mat(d, "diag5"))
+    M = P.L1JacobiData(m_diag=np.ones(5))
+    e0 = np.array([1.0, -1.0, 2.0, 0.5, -0.25])
+    for k in (1, 2, 4, 6):
+        cfg = P.PolySmootherConfig(family="opt_cheb1", degree=k, a=0.1)
+        assert np.array_equal(P.smoother_error_apply(cfg, A, M, e0),
+                              d[f"diag5_opt_cheb1_a0.1_k{k}_err"])
+    # cheb4 k=1 with M = A: p_1(1) = -1/3 (tests/test_smoothers.py:81-90)
+    A = P.CsrMatrix.from_dense(np.diag([2.0, 3.0]))
+    M = P.L1JacobiData(m_diag=np.array([2.0, 3.0]))
+    e0 = np.array([1.0, -2.0])
+    out = P.smoother_error_apply(P.PolySmootherConfig(family="cheb4", degree=1), A, M, e0)
+    assert np.allclose(out, -e0 / 3.0, atol=1e-14)
+
+
+def test_smoother_spmv_count_and_errors(P):
+    A, d = small_csr(P, "tridiag20")
+    M = P.l1_jacobi_diag(A)
+    for fam in FAMILIES:
+        for k in (1, 2, 5):
+            P.reset_spmv_count()
+            P.smoother_apply(P.PolySmootherConfig(family=fam, degree=k), A, M, np.ones(20), np.zeros(20))
+            assert P.spmv_count() == k
+    with pytest.raises(ValueError):
+        P.smoother_apply(P.PolySmootherConfig(family="cheb4", degree=2), A, M, np.ones(21), np.zeros(20))
+
+
+def test_smoother_torch_inputs_and_alias(P):
+    import torch
+
+    A, d = small_csr(P, "p3d8")
+    M = P.L1JacobiData(m_diag=d["p3d8_m"])
+    b = torch.tensor(d["p3d8_b"], device="cuda")
+    x0 = torch.tensor(d["p3d8_x0"], device="cuda")
+    cfg = P.PolySmootherConfig(family="opt_cheb1", degree=4)
+    out = P.smoother_apply(cfg, A, M, b, x0)
+    assert isinstance(out, torch.Tensor) and out.is_cuda
+    assert np.array_equal(out.cpu().numpy(), d["p3d8_opt_cheb1_k4_x0"])
+    assert np.array_equal(x0.cpu().numpy(), d["p3d8_x0"])  # x0 not mutated
+
+
+def test_fused_update_bitwise(P, rng):
+    for n in (1, 7, 1000, 100_000):
+        s, r, d, x = (rng.standard_normal(n) for _ in range(4))
+        rho, rho_prev, c = rng.standard_normal(3)
+        r2, d2, x2 = r.copy(), d.copy(), x.copy()
+        P.fused_update(rho, rho_prev, c, s, r, d, x)
+        r2 -= s
+        d2 = rho * rho_prev * d2 + c * r2
+        x2 += d2
+        assert np.array_equal(r, r2) and np.array_equal(d, d2) and np.array_equal(x, x2)
+    with pytest.raises(ValueError):
+        P.fused_update(1.0, 1.0, 1.0, np.ones(2), np.ones(3), np.ones(3), np.ones(3))
+
+
+@pytest.mark.parametrize("m", [2, 3, 5, 8, 13, 33])
+def test_device_poisson_generator(P, m):
+    A, _ = P.poisson3d(m)
+    D = P.poisson3d_device(m)
+    assert D.nnz == A.nnz
+    B = D.to_csr()
+    assert np.array_equal(B.row_ptr, A.row_ptr)
+    assert np.array_equal(B.col_idx, A.col_idx)
+    assert np.array_equal(B.values, A.values)
+    m_host = P.l1_jacobi_diag(A).m_diag
+    assert np.array_equal(D.l1_diag().cpu().numpy(), m_host)
+    A27, _ = P.poisson3d_27(m)
+    D27 = P.poisson3d_device(m, stencil=27)
+    B = D27.to_csr()
+    assert np.array_equal(B.col_idx, A27.col_idx) and np.array_equal(B.values, A27.values)
+    assert np.array_equal(D27.l1_diag().cpu().numpy(), P.l1_jacobi_diag(A27).m_diag)
+
+
+def test_device_poisson_row_block(P):
+    m = 9
+    A, _ = P.poisson3d(m)
+    D = P.poisson3d_device(m, row_begin=100, row_end=500)
+    B = D.to_csr()
+    assert np.array_equal(B.col_idx, A.col_idx[A.row_ptr[100]:A.row_ptr[500]])
+    assert np.array_equal(D.l1_diag().cpu().numpy(), P.l1_jacobi_diag(A).m_diag[100:500])
+
+
+@pytest.mark.parametrize("name", SMALL)
+def test_device_l1_diag_of_uploaded_csr(P, name):
+    A, d = small_csr(P, name)
+    assert np.array_equal(A.device().l1_diag().cpu().numpy(), d[name + "_m"])
+
+
+def golden_hierarchy(P, prefix, cfg):
+    d = golden("hier_small.npz")
+    L = int(d[prefix + "_nlev"][0])
+    levels = []
+    for l in range(L):
+        A = P.CsrMatrix(*golden_mat(d, f"{prefix}_A{l}"))
+        lv = P.Level(A=A, M=P.L1JacobiData(m_diag=d[f"{prefix}_M{l}"]), smoother=cfg)
+        if l < L - 1:
+            lv.P = P.CsrMatrix(*golden_mat(d, f"{prefix}_P{l}"))
+            lv._Pt = P.CsrMatrix(*golden_mat(d, f"{prefix}_R{l}"))
+        levels.append(lv)
+    return P.AmgHierarchy(levels=levels), d
+
+
+@pytest.mark.parametrize("prefix", ["sa16", "mt8", "mt16"])
+def test_vcycle_bitwise_vs_reference(P, prefix):
+    h, d = golden_hierarchy(P, prefix, P.PolySmootherConfig(family="cheb4", degree=4))
+    r = d[prefix + "_r"]
+    for fam in FAMILIES:
+        for k in (1, 2, 4, 6):
+            cfg = P.PolySmootherConfig(family=fam, degree=k)
+            for lv in h.levels:
+                lv.smoother = cfg
+            assert np.array_equal(P.vcycle_apply(h, r), d[f"{prefix}_vc_{fam}_k{k}"]), (fam, k)
+
+
+def test_vcycle_zero_and_linearity(P, rng):
+    h, d = golden_hierarchy(P, "sa16", P.PolySmootherConfig(family="opt_cheb1", degree=4))
+    n = h.levels[0].A.nrows
+    assert np.array_equal(P.vcycle_apply(h, np.zeros(n)), np.zeros(n))
+    r, s = rng.standard_normal(n), rng.standard_normal(n)
+    lhs = P.vcycle_apply(h, 0.7 * r - 1.3 * s)
+    rhs = 0.7 * P.vcycle_apply(h, r) - 1.3 * P.vcycle_apply(h, s)
+    assert np.allclose(lhs, rhs, atol=1e-12 * max(1.0, np.abs(rhs).max()))
+    with pytest.raises(ValueError):
+        P.vcycle_apply(h, np.zeros(n + 1))
+
+
+@pytest.mark.parametrize("prefix", ["sa16", "mt8", "mt16"])
+def test_pcg_iterations_vs_reference(P, prefix):
+    h, d = golden_hierarchy(P, prefix, P.PolySmootherConfig(family="cheb4", degree=4))
+    n = h.levels[0].A.nrows
+    A = h.levels[0].A
+    for fam in FAMILIES:
+        for k in (1, 2, 4, 6):
+            cfg = P.PolySmootherConfig(family=fam, degree=k)
+            for lv in h.levels:
+                lv.smoother = cfg
+            x, rep = P.solve(A, np.ones(n), precond=P.as_vcycle_preconditioner(h),
+                             cfg=P.KrylovConfig(tol=1e-6))
+            want = int(d[f"{prefix}_pcg_{fam}_k{k}_iters"][0])
+            assert rep.converged and abs(rep.iterations - want) <= 1, (fam, k, rep.iterations, want)
+            assert rep.iterations == want  # observed exactly equal
+            assert np.allclose(rep.residual_history, d[f"{prefix}_pcg_{fam}_k{k}_hist"], rtol=1e-8)
+            assert np.allclose(x, d[f"{prefix}_pcg_{fam}_k{k}_x"], rtol=1e-8, atol=1e-12)
+            assert rep.spmv_count == rep.iterations + 1
+
+
+def test_pcg_plain_and_fcg_and_breakdown(P):
+    A = P.CsrMatrix.identity(5)
+    b = np.arange(1.0, 6.0)
+    x, rep = P.solve(A, b)
+    assert rep.converged and rep.iterations == 1 and np.allclose(x, b)
+    x, rep = P.solve(A, np.zeros(5))
+    assert rep.converged and rep.iterations == 0 and np.array_equal(x, np.zeros(5))
+    Ai = P.CsrMatrix.from_dense(np.diag([1.0, -1.0]))
+    _, rep = P.solve(Ai, np.array([1.0, 1.0]), cfg=P.KrylovConfig(tol=1e-12))
+    assert rep.breakdown and not rep.converged
+    h, d = golden_hierarchy(P, "mt8", P.PolySmootherConfig(family="opt_cheb1", degree=4))
+    n = h.levels[0].A.nrows
+    its = {}
+    for variant in ("pcg", "fcg"):
+        _, rep = P.solve(h.levels[0].A, np.ones(n), precond=P.as_vcycle_preconditioner(h),
+                         cfg=P.KrylovConfig(variant=variant))
+        assert rep.converged
+        its[variant] = rep.iterations
+    assert abs(its["pcg"] - its["fcg"]) <= 1
+    # warm start from the solution: zero iterations
+    x, _ = P.solve(h.levels[0].A, np.ones(n), precond=P.as_vcycle_preconditioner(h),
+                   cfg=P.KrylovConfig(tol=1e-12))
+    _, rep = P.solve(h.levels[0].A, np.ones(n), precond=P.as_vcycle_preconditioner(h), x0=x,
+                     cfg=P.KrylovConfig(tol=1e-10))
+    assert rep.iterations == 0
+
+
+def test_pcg_with_smoother_preconditioner(P):
+    A, _ = P.poisson3d(8)
+    M = P.l1_jacobi_diag(A)
+    pre = P.as_preconditioner(P.PolySmootherConfig(family="opt_cheb1", degree=4), A, M)
+    b = np.ones(A.nrows)
+    x, rep = P.solve(A, b, precond=pre, cfg=P.KrylovConfig(tol=1e-8))
+    assert rep.converged
+    assert np.linalg.norm(b - A.to_dense() @ x) / np.linalg.norm(b) <= 1e-8
+    with pytest.raises(TypeError):
+        P.solve(A, b, precond=lambda r: r)
+
+
+def test_dense_direct_coarse(P):
+    h, d = golden_hierarchy(P, "sa16", P.PolySmootherConfig(family="opt_cheb1", degree=4))
+    h.coarse_solver = "dense_direct"
+    n = h.levels[0].A.nrows
+    r = d["sa16_r"]
+    got = P.vcycle_apply(h, r)
+    lv = [{"A": (l.A.row_ptr, l.A.col_idx, l.A.values), "m": l.M.m_diag} for l in h.levels]
+    # host reference: same V-cycle with an exact coarse solve
+    import scipy.linalg
+
+    Ac = h.levels[-1].A.to_dense()
+
+    def vc(l, rl):
+        Al = h.levels[l]
+        if l == len(h.levels) - 1:
+            return scipy.linalg.cho_solve(scipy.linalg.cho_factor(Ac, lower=True), rl)
+        kw = dict(a=Al.smoother.a)
+        x = oracle.smoother_apply("opt_cheb1", 4, Al.A.row_ptr, Al.A.col_idx, Al.A.values,
+                                  Al.M.m_diag, rl, None, **kw)
+        res = rl - oracle.spmv(Al.A.row_ptr, Al.A.col_idx, Al.A.values, Al.A.ncols, x)
+        R = Al.restrict_op()
+        xc = vc(l + 1, oracle.spmv(R.row_ptr, R.col_idx, R.values, R.ncols, res))
+        x = x + oracle.spmv(Al.P.row_ptr, Al.P.col_idx, Al.P.values, Al.P.ncols, xc)
+        return oracle.smoother_apply("opt_cheb1", 4, Al.A.row_ptr, Al.A.col_idx, Al.A.values,
+                                     Al.M.m_diag, rl, x, **kw)
+
+    want = vc(0, r)
+    assert np.allclose(got, want, rtol=1e-12, atol=1e-12 * np.abs(want).max())
+
+
+@pytest.mark.parametrize("m", [48, 64])
+def test_fine_level_smoother_bitwise_vs_oracle(P, m):
+    A, _ = P.poisson3d(m)
+    n = A.nrows
+    M = P.l1_jacobi_diag(A)
+    b = np.random.default_rng(0).standard_normal(n)
+    x0 = np.random.default_rng(1).standard_normal(n)
+    params = smoother_params()
+    for fam in FAMILIES:
+        for k in (1, 4, 6):
+            cfg = P.PolySmootherConfig(family=fam, degree=k)
+            beta = cfg.beta.beta if cfg.family == "opt_cheb4" else None
+            want = oracle.smoother_apply(cfg.family, k, A.row_ptr, A.col_idx, A.values, M.m_diag,
+                                         b, x0, a=cfg.a or 0.0, beta=beta)
+            assert np.array_equal(P.smoother_apply(cfg, A, M, b, x0), want), (fam, k)
+
+
+def test_256cube_generated_smoother_bitwise_vs_oracle(P):
+    """Full BASELINE size (256^3, 117M nnz): device-generated matrix, every
+    family at k=4, bitwise against the multi-threaded C oracle."""
+    import torch
+
+    m = 256
+    D = P.poisson3d_device(m)
+    A, _ = P.poisson3d(m)
+    n = A.nrows
+    M = P.L1JacobiData(m_diag=D.l1_diag())
+    b = np.random.default_rng(0).standard_normal(n)
+    x0 = np.random.default_rng(1).standard_normal(n)
+    m_host = D.l1_diag().cpu().numpy()
+    oracle.set_threads(oracle.max_threads())
+    try:
+        for fam in FAMILIES:
+            cfg = P.PolySmootherConfig(family=fam, degree=4)
+            beta = cfg.beta.beta if cfg.family == "opt_cheb4" else None
+            got = P.smoother_apply(cfg, D, M, torch.tensor(b, device="cuda"),
+                                   torch.tensor(x0, device="cuda")).cpu().numpy()
+            want = oracle.smoother_apply(cfg.family, 4, A.row_ptr, A.col_idx, A.values, m_host,
+                                         b, x0, a=cfg.a or 0.0, beta=beta)
+            assert np.array_equal(got, want), fam
+    finally:
+        oracle.set_threads(1)

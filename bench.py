@@ -18,6 +18,7 @@ blocks... (current round: independent per-rank fine levels).
 from __future__ import annotations
 
 import argparse
+import datetime
 import json
 import os
 import statistics
@@ -56,7 +57,7 @@ def peaks():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -66,16 +67,25 @@ class ClockSampler:
         self.f = None
 
     def start(self):
+        """Start sampling; returns once the first sample has been written."""
         try:
             self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", "100"],
                 stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
+            return
+        t0 = time.time()
+        while time.time() - t0 < 10 and self.proc.poll() is None:
+            if os.path.getsize(self.f.name) > 0:
+                break
+            time.sleep(0.05)
 
-    def stop(self):
+    def stop(self, t_begin=None, t_end=None):
+        """Stop; summarise the samples taken in [t_begin, t_end] (wall clock),
+        or all samples when the window caught none (a very short region)."""
         if self.proc is None:
             return None
         self.proc.terminate()
@@ -88,18 +98,36 @@ class ClockSampler:
         with open(self.f.name) as fh:
             for line in fh:
                 p = [x.strip() for x in line.split(",")]
-                if len(p) >= 8:
+                if len(p) >= 9:
+                    try:
+                        p[0] = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
+                    except ValueError:
+                        continue
                     rows.append(p)
         os.unlink(self.f.name)
+        window = "timed region"
+        if t_begin is not None:
+            inside = [r for r in rows if t_begin <= r[0] <= t_end]
+            if inside:
+                rows = inside
+            else:
+                window = "whole run (timed region shorter than the sampling period)"
         if not rows:
             return None
-        sm = [float(r[0]) for r in rows if r[0].replace(".", "").isdigit()]
-        mx = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+
+        def num(v):
+            try:
+                return float(v)
+            except ValueError:
+                return None
+
+        sm = [num(r[1]) for r in rows if num(r[1]) is not None]
+        mx = [num(r[2]) for r in rows if num(r[2]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if "Active" in r[4 + i]})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(rows)}
+                "samples": len(rows), "window": window}
 
 
 # ---------------------------------------------------------------- distributed
@@ -245,23 +273,25 @@ def run_b200(args):
             dist.barrier()
         torch.cuda.synchronize()
 
+    sampler = ClockSampler(dev)
+    sampler.start()
     for _ in range(args.warmup):
         step()
     barrier()
-    sampler = ClockSampler(dev)
-    sampler.start()
     per = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
             for _ in cfgs] for _ in range(args.steps)]
     t_start = torch.cuda.Event(enable_timing=True)
     t_end = torch.cuda.Event(enable_timing=True)
     launches0 = c.launches()
+    wall0 = time.time()
     t_start.record(c.stream)
     for s in range(args.steps):
         step(per[s])
     t_end.record(c.stream)
     torch.cuda.synchronize()
+    wall1 = time.time()
     launches = c.launches() - launches0
-    clocks = sampler.stop()
+    clocks = sampler.stop(wall0, wall1)
     ms = t_start.elapsed_time(t_end)
     if ws > 1:
         t = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -338,7 +368,7 @@ def run_b200(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--m", type=int, default=256)

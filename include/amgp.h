@@ -158,6 +158,34 @@ int amgp_sell_pack_host(int64_t nrows, const int64_t *row_ptr, const int64_t *co
  * 2 rho_j/delta) for j=1..degree-1 at coef[1+2(j-1)].  */
 int amgp_smoother_coefficients(const amgp_smoother_cfg *cfg, double *coef);
 
+/* ---- native host setup (amg.py:97-287), bit-exact with the reference ----
+ * Host CSR in / out (int64 indices, f64 values).  Results of variable size
+ * come back as an opaque amgp_hcsr (query with amgp_hcsr_info, copy out with
+ * amgp_hcsr_copy, release with amgp_hcsr_free). */
+typedef struct amgp_hcsr amgp_hcsr;
+int amgp_setup_set_threads(int threads);
+int amgp_hcsr_info(const amgp_hcsr *h, int64_t *nrows, int64_t *ncols, int64_t *nnz);
+int amgp_hcsr_copy(const amgp_hcsr *h, int64_t *row_ptr, int64_t *col_idx, double *values);
+int amgp_hcsr_free(amgp_hcsr *h);
+/* amg.py:102-149 sa_aggregate -> agg[n], *n_agg */
+int amgp_setup_sa_aggregate(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                            const double *values, double theta, int64_t *agg, int64_t *n_agg);
+/* amg.py:152-191 matching_aggregate -> agg[n], *n_agg */
+int amgp_setup_matching_aggregate(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                                  const double *values, int sweeps, int64_t *agg,
+                                  int64_t *n_agg);
+/* amg.py:219-226 smooth_prolongator(A, P_hat(agg), omega) */
+int amgp_setup_smooth_prolongator(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                                  const double *values, const int64_t *agg, int64_t n_agg,
+                                  double omega, amgp_hcsr **P);
+/* amg.py:229-235 galerkin_rap(A, P) */
+int amgp_setup_galerkin(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                        const double *values, int64_t nc, const int64_t *p_row_ptr,
+                        const int64_t *p_col_idx, const double *p_values, amgp_hcsr **Ac);
+/* host y = A x in stored order (the power iteration of amg.py:194-216) */
+int amgp_setup_spmv(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
+                    const double *values, const double *x, double *y);
+
 #ifdef __cplusplus
 }
 #endif

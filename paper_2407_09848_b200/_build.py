@@ -33,7 +33,7 @@ LIBS = ["-lnccl"]
 
 
 def sources():
-    return sorted(glob.glob(os.path.join(CSRC, "*.cu")))
+    return sorted(glob.glob(os.path.join(CSRC, "*.cu")) + glob.glob(os.path.join(CSRC, "*.cpp")))
 
 
 def headers():
@@ -55,7 +55,7 @@ def build(force=False, verbose=False):
     os.makedirs(odir, exist_ok=True)
     procs = []
     for src in sources():
-        obj = os.path.join(odir, os.path.basename(src).replace(".cu", ".o"))
+        obj = os.path.join(odir, os.path.splitext(os.path.basename(src))[0] + ".o")
         cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "--shared"], "-c",
                src, "-o", obj]
         if verbose:

@@ -90,6 +90,17 @@ _SIGS = {
     "amgp_sell_pack_host": (C.c_int, [C.c_int64, _P64, _P64, _PD, _P64, _P64, _P64,
                                        C.POINTER(C.c_int32), _PD]),
     "amgp_smoother_coefficients": (C.c_int, [C.POINTER(SmootherCfg), _PD]),
+    "amgp_setup_set_threads": (C.c_int, [C.c_int]),
+    "amgp_hcsr_info": (C.c_int, [_VP, _P64, _P64, _P64]),
+    "amgp_hcsr_copy": (C.c_int, [_VP, _P64, _P64, _PD]),
+    "amgp_hcsr_free": (C.c_int, [_VP]),
+    "amgp_setup_sa_aggregate": (C.c_int, [C.c_int64, _P64, _P64, _PD, C.c_double, _P64, _P64]),
+    "amgp_setup_matching_aggregate": (C.c_int, [C.c_int64, _P64, _P64, _PD, C.c_int, _P64, _P64]),
+    "amgp_setup_smooth_prolongator": (C.c_int, [C.c_int64, _P64, _P64, _PD, _P64, C.c_int64,
+                                                 C.c_double, C.POINTER(_VP)]),
+    "amgp_setup_galerkin": (C.c_int, [C.c_int64, _P64, _P64, _PD, C.c_int64, _P64, _P64, _PD,
+                                       C.POINTER(_VP)]),
+    "amgp_setup_spmv": (C.c_int, [C.c_int64, _P64, _P64, _PD, _PD, _PD]),
 }
 
 _lib = None
@@ -242,7 +253,13 @@ def like(t, ref):
     """Return device result t in the container type of the input ref:
     CUDA tensor -> as is; host tensor -> host tensor; else numpy."""
     if is_torch(ref):
-        return t if ref.is_cuda else t.cpu()
+        if ref.is_cuda:
+            return t
+        if ref.is_pinned():  # pinned in -> pinned out (cached pinned allocator, DMA copy)
+            out = t.new_empty(t.shape, device="cpu", pin_memory=True)
+            out.copy_(t)
+            return out
+        return t.cpu()
     return to_host(t)
 
 

@@ -22,7 +22,8 @@ from paper_2407_09848_b200 import _native as N
 
 def header_symbols():
     text = open(os.path.join(REPO, "include", "amgp.h")).read()
-    return sorted(set(re.findall(r"\b(amgp_[a-z0-9_]+)\s*\(", text)))
+    decl = r"^\s*(?:int|const char \*)\s*(amgp_[a-z0-9_]+)\s*\("
+    return sorted(set(re.findall(decl, text, flags=re.M)))
 
 
 def test_library_exports_every_header_symbol():

@@ -237,6 +237,65 @@ def cpu_baseline(m):
                       f"({tot_t:.1f} s)"}
 
 
+def solve_bench(m, kind="smoothed_aggregation", cpu=True):
+    """PCG + AMG V-cycle solve (BASELINE metric part 2) on poisson3d(m):
+    native host setup, then per smoother family (k=4) one device solve at
+    rtol 1e-6 timed with CUDA events on the library stream; the C oracle
+    solves the same hierarchy on the host for the CPU column."""
+    import torch
+
+    import paper_2407_09848_b200 as P
+    from paper_2407_09848_b200 import _native as N
+
+    A, b = P.poisson3d(m)
+    t0 = time.perf_counter()
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+                          smoother=P.PolySmootherConfig(family="opt_cheb1", degree=4))
+    setup_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    D = h.device()
+    upload_s = time.perf_counter() - t0
+    c = D.ctx
+    bd = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
+    cfg_k = P.KrylovConfig(tol=1e-6, itmax=1000)
+    out = {"m": m, "n": A.nrows, "coarsening": kind, "levels": [lv.A.nrows for lv in h.levels],
+           "operator_complexity": h.operator_complexity(), "setup_s": setup_s,
+           "upload_s": upload_s, "tol": 1e-6, "results": {}}
+    for fam in ("opt_cheb1", "cheb4", "opt_cheb4", "l1_jacobi"):
+        cfg = P.PolySmootherConfig(family=fam, degree=4)
+        for lv in h.levels:
+            lv.smoother = cfg
+        pre = P.as_vcycle_preconditioner(h)
+        P.solve(A, bd, precond=pre, cfg=cfg_k)  # warm-up (graph capture)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(c.stream)
+        x, rep = P.solve(A, bd, precond=pre, cfg=cfg_k)
+        e1.record(c.stream)
+        torch.cuda.synchronize()
+        out["results"][fam] = {"iterations": rep.iterations, "final_relres": rep.final_relres,
+                               "solve_s": e0.elapsed_time(e1) / 1e3, "wall_s": rep.elapsed_s}
+    if cpu:
+        sys.path.insert(0, os.path.join(REPO, "oracle"))
+        import oracle
+
+        lv = [{"A": (l.A.row_ptr, l.A.col_idx, l.A.values), "m": l.M.m_diag,
+               **({"P": (l.P.row_ptr, l.P.col_idx, l.P.values),
+                   "R": (l.restrict_op().row_ptr, l.restrict_op().col_idx, l.restrict_op().values)}
+                  if l.P is not None else {})} for l in h.levels]
+        cfg = P.PolySmootherConfig(family="opt_cheb1", degree=4)
+        oh = oracle.Hierarchy(lv, "opt_cheb1", 4, a=cfg.a)
+        threads = oracle.max_threads()
+        oracle.set_threads(threads)
+        t0 = time.perf_counter()
+        _, it, rr, conv, brk, _ = oracle.pcg(lv[0]["A"], np.ones(A.nrows), oh, tol=1e-6)
+        out["cpu_opt_cheb1"] = {"iterations": it, "final_relres": rr,
+                                "solve_s": time.perf_counter() - t0, "cores": threads,
+                                "kind": "port"}
+        oracle.set_threads(1)
+    return out
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -358,6 +417,8 @@ def run_b200(args):
         }
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_m)
+        if ws == 1 and args.solve_m > 0:
+            line["solve"] = solve_bench(args.solve_m, cpu=not args.no_cpu_baseline)
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
@@ -374,6 +435,8 @@ def main():
     ap.add_argument("--m", type=int, default=256)
     ap.add_argument("--cpu-m", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--solve-m", type=int, default=128,
+                    help="grid size of the PCG+AMG solve section (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

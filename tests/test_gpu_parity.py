@@ -341,3 +341,69 @@ def test_256cube_generated_smoother_bitwise_vs_oracle(P):
             assert np.array_equal(got, want), fam
     finally:
         oracle.set_threads(1)
+
+
+def _sha(a):
+    import hashlib
+
+    return hashlib.sha256(np.ascontiguousarray(a, dtype=np.float64).tobytes()).hexdigest()
+
+
+@pytest.mark.parametrize("m", [32, 64])
+@pytest.mark.parametrize("kind", ["smoothed_aggregation", "pairwise_matching"])
+def test_native_hierarchy_vcycle_digest_vs_reference(P, m, kind):
+    """Native setup + device V-cycle reproduce the reference's V-cycle output
+    bit for bit (SHA-256 of the reference's vcycle_apply at 32^3 / 64^3)."""
+    ref = golden("hashes.json")[f"p3d{m}_{kind}"]
+    A, b = P.poisson3d(m)
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+                          smoother=P.PolySmootherConfig(family="cheb4", degree=4))
+    r = np.random.default_rng(5).standard_normal(A.nrows)
+    for fam in FAMILIES:
+        cfg = P.PolySmootherConfig(family=fam, degree=4)
+        for lv in h.levels:
+            lv.smoother = cfg
+        assert _sha(P.vcycle_apply(h, r)) == ref["vcycle"][fam], (m, kind, fam)
+
+
+@pytest.mark.parametrize("kind", ["smoothed_aggregation", "pairwise_matching"])
+def test_pcg_iteration_table_32cube(P, kind):
+    """PCG+AMG iterations at rtol 1e-6 equal the reference's table."""
+    ref = golden("hashes.json")[f"p3d32_{kind}"]
+    A, b = P.poisson3d(32)
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+                          smoother=P.PolySmootherConfig(family="cheb4", degree=4))
+    for fam in FAMILIES:
+        for k in range(1, 7):
+            cfg = P.PolySmootherConfig(family=fam, degree=k)
+            for lv in h.levels:
+                lv.smoother = cfg
+            _, rep = P.solve(A, b, precond=P.as_vcycle_preconditioner(h), cfg=P.KrylovConfig(tol=1e-6))
+            want = ref["pcg"][f"{fam}_k{k}"]
+            assert rep.converged
+            assert abs(rep.iterations - want["iterations"]) <= 1, (fam, k, rep.iterations, want)
+            assert rep.iterations == want["iterations"]  # observed exactly equal
+            assert rep.final_relres == pytest.approx(want["final_relres"], rel=1e-6)
+
+
+def test_smoother_digests_32cube_all_levels(P):
+    ref = golden("hashes.json")["p3d32_smoothed_aggregation"]
+    A, b = P.poisson3d(32)
+    h = P.build_hierarchy(A, smoother=P.PolySmootherConfig(family="cheb4", degree=4))
+    n = A.nrows
+    bb = np.random.default_rng(0).standard_normal(n)
+    x0 = np.random.default_rng(1).standard_normal(n)
+    M = h.levels[0].M
+    for fam in FAMILIES:
+        for k in range(1, 7):
+            cfg = P.PolySmootherConfig(family=fam, degree=k)
+            assert _sha(P.smoother_apply(cfg, A, M, bb, x0)) == ref["smoother"][f"{fam}_k{k}_x0"]
+            assert _sha(P.smoother_apply(cfg, A, M, bb, np.zeros(n))) == ref["smoother"][f"{fam}_k{k}_zero"]
+    for l in (1, 2):
+        Al, Ml = h.levels[l].A, h.levels[l].M
+        nl = Al.nrows
+        bl = np.random.default_rng(0).standard_normal(nl)
+        xl = np.random.default_rng(1).standard_normal(nl)
+        for fam in FAMILIES:
+            cfg = P.PolySmootherConfig(family=fam, degree=4)
+            assert _sha(P.smoother_apply(cfg, Al, Ml, bl, xl)) == ref["smoother"][f"L{l}_{fam}_k4_x0"]

@@ -13,7 +13,7 @@
 #include <algorithm>
 #include <vector>
 
-#include "amgp_common.cuh"
+#include "rows.cuh"
 
 // ---------------------------------------------------------------- host packing
 extern "C" int amgp_sell_pack_host(int64_t nrows, const int64_t *row_ptr,
@@ -382,43 +382,28 @@ extern "C" int amgp_mat_l1_diag(amgp_mat *A, double *m_dev) {
 }
 
 // ---------------------------------------------------------------- SpMV kernels
-#define ROWS_PER_BLOCK 256
-#define SLICES_PER_BLOCK (ROWS_PER_BLOCK / 32)
-
-// MODE 0: y = A x ; MODE 1: y = r - A x ; MODE 2: y = y + A x  (x += P xc)
+// MODE 0: y = A x ; MODE 1: y = r - A x (amg.py:311) ; MODE 2: y = y + A x (amg.py:314)
 template <int MODE>
-__global__ void __launch_bounds__(ROWS_PER_BLOCK)
-k_spmv(SellView A, const double *__restrict__ x, const double *__restrict__ r, double *y) {
-    const int64_t s = (int64_t)blockIdx.x * SLICES_PER_BLOCK + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (s >= A.nslices) return;
-    const double sum = sell_row_dot<8>(A, s, lane, x);
-    const int64_t row = s * 32 + lane;
-    if (row >= A.nrows) return;
-    if (MODE == 0) y[row] = sum;
-    else if (MODE == 1) y[row] = __dsub_rn(r[row], sum);   // amg.py:311
-    else y[row] = __dadd_rn(y[row], sum);                  // amg.py:314
-}
-
-template <int MODE>
-static int spmv_launch(amgp_ctx *ctx, const amgp_mat *A, const double *x, const double *r,
-                       double *y) {
-    if (A->nslices == 0) return AMGP_OK;
-    k_spmv<MODE><<<grid_for(A->nslices, SLICES_PER_BLOCK), ROWS_PER_BLOCK, 0, ctx->stream>>>(
-        view_of(A), x, r, y);
-    AMGP_CHECK_LAUNCH(ctx);
-    return AMGP_OK;
-}
+struct SpmvEpi {
+    static constexpr bool kSpmv = true;
+    const double *__restrict__ r;
+    double *y;
+    __device__ __forceinline__ void operator()(int64_t row, double sum) const {
+        if (MODE == 0) y[row] = sum;
+        else if (MODE == 1) y[row] = __dsub_rn(r[row], sum);
+        else y[row] = __dadd_rn(y[row], sum);
+    }
+};
 
 int spmv_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y) {
-    return spmv_launch<0>(ctx, A, x, nullptr, y);
+    return launch_rows(ctx, A, x, SpmvEpi<0>{nullptr, y});
 }
 int residual_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *r, const double *x,
                      double *res) {
-    return spmv_launch<1>(ctx, A, x, r, res);
+    return launch_rows(ctx, A, x, SpmvEpi<1>{r, res});
 }
 int prolong_add_enqueue(amgp_ctx *ctx, const amgp_mat *P, const double *xc, double *x) {
-    return spmv_launch<2>(ctx, P, xc, nullptr, x);
+    return launch_rows(ctx, P, xc, SpmvEpi<2>{nullptr, x});
 }
 
 extern "C" int amgp_spmv(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y) {

@@ -179,19 +179,35 @@ __global__ void k_scale_zero(int64_t n, double *x) {
 }
 
 namespace {
-struct PcgWork {
+struct PcgWork {  // views into the context's cached PCG workspace
     double *partial = nullptr;
     unsigned *ticket = nullptr;
     double *r = nullptr, *z = nullptr, *d = nullptr, *Ad = nullptr;
-    ~PcgWork() {
-        cudaFree(partial);
-        cudaFree(ticket);
-        cudaFree(r);
-        cudaFree(z);
-        cudaFree(d);
-        cudaFree(Ad);
-    }
 };
+
+// Grow-only workspace cached on the context: cudaMalloc/cudaFree per solve
+// would synchronise the device inside the caller's pipeline.
+int pcg_workspace(amgp_ctx *ctx, int64_t n, PcgWork *w) {
+    const int64_t need = 4 * std::max<int64_t>(n, 1) + 2 * RGRID_MAX + 8;
+    if (ctx->red_partial_n < need) {
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(ctx->red_partial);
+        ctx->red_partial = nullptr;
+        ctx->red_partial_n = 0;
+        AMGP_CUDA(cudaMalloc(&ctx->red_partial, need * sizeof(double)));
+        ctx->red_partial_n = need;
+        AMGP_CUDA(cudaMemsetAsync(ctx->red_partial, 0, need * sizeof(double), ctx->stream));
+    }
+    double *p = ctx->red_partial;
+    const int64_t nn = std::max<int64_t>(n, 1);
+    w->ticket = (unsigned *)p;  // 8 doubles of room for the tickets (zeroed once)
+    w->partial = p + 8;
+    w->r = w->partial + 2 * RGRID_MAX;
+    w->z = w->r + nn;
+    w->d = w->z + nn;
+    w->Ad = w->d + nn;
+    return AMGP_OK;
+}
 }  // namespace
 
 static unsigned rgrid(int64_t n) {
@@ -221,13 +237,7 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
 
     PcgWork w;
     const size_t nb = (size_t)std::max<int64_t>(n, 1) * sizeof(double);
-    AMGP_CUDA(cudaMalloc(&w.partial, 2 * RGRID_MAX * sizeof(double)));
-    AMGP_CUDA(cudaMalloc(&w.ticket, 4 * sizeof(unsigned)));
-    AMGP_CUDA(cudaMalloc(&w.r, nb));
-    AMGP_CUDA(cudaMalloc(&w.z, nb));
-    AMGP_CUDA(cudaMalloc(&w.d, nb));
-    AMGP_CUDA(cudaMalloc(&w.Ad, nb));
-    AMGP_CUDA(cudaMemsetAsync(w.ticket, 0, 4 * sizeof(unsigned), st));
+    AMGP_TRY(pcg_workspace(ctx, n, &w));
     const unsigned g = rgrid(n);
     const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(A->nslices, RB / 32), RGRID_MAX));
 
@@ -285,6 +295,23 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     k_pcg_dot_init<2><<<g, RB, 0, st>>>(n, w.r, w.z, w.partial, w.ticket, sc);  // rz
     AMGP_CHECK_LAUNCH(ctx);
 
+    // next preconditioner application + direction update (krylov.py:108-119)
+    auto next_direction = [&]() -> int {
+        AMGP_TRY(precond());
+        if (fcg) k_pcg_dot<true><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
+        else k_pcg_dot<false><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
+        AMGP_CHECK_LAUNCH(ctx);
+        if (fcg) k_pcg_dir<true><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
+        else k_pcg_dir<false><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
+        AMGP_CHECK_LAUNCH(ctx);
+        return AMGP_OK;
+    };
+    struct Ev {
+        cudaEvent_t e = nullptr;
+        ~Ev() { if (e) cudaEventDestroy(e); }
+    } ev;
+    AMGP_CUDA(cudaEventCreateWithFlags(&ev.e, cudaEventDisableTiming));
+    double rel_prev = relres, rel_prev2 = -1.0;
     for (int it = 1; it <= itmax; it++) {
         if (fcg) k_pcg_spmv_dot<true><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
         else k_pcg_spmv_dot<false><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
@@ -293,25 +320,18 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
         k_pcg_update<<<g, RB, 0, st>>>(n, x, w.r, w.d, w.Ad, w.partial, w.ticket, sc);
         AMGP_CHECK_LAUNCH(ctx);
         AMGP_CUDA(cudaMemcpyAsync(hs, sc, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
-        cudaEvent_t ev;
-        AMGP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-        cudaEventRecord(ev, st);
-        // speculative: next preconditioner application and direction update
-        int s1 = precond();
-        if (s1 == AMGP_OK) {
-            if (fcg) k_pcg_dot<true><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
-            else k_pcg_dot<false><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
-            cudaError_t e1 = cudaGetLastError();
-            if (fcg) k_pcg_dir<true><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
-            else k_pcg_dir<false><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
-            cudaError_t e2 = cudaGetLastError();
-            if (e1 != cudaSuccess || e2 != cudaSuccess) s1 = amgp_cuda_fail(e1 != cudaSuccess ? e1 : e2, "pcg kernels", __FILE__, __LINE__);
-            ctx->launches.fetch_add(2);
+        AMGP_CUDA(cudaEventRecord(ev.e, st));
+        // While the host waits for relres, keep the GPU busy with the next
+        // V-cycle -- unless the residual history predicts convergence at this
+        // check (then the V-cycle would be wasted work).  Harmless either
+        // way: x and r are final before the event.
+        bool spec = true;
+        if (rel_prev2 > 0.0) {
+            const double ratio = rel_prev / rel_prev2;
+            if (rel_prev * ratio <= 2.0 * tol) spec = false;
         }
-        cudaError_t es = cudaEventSynchronize(ev);
-        cudaEventDestroy(ev);
-        if (s1 != AMGP_OK) return s1;
-        if (es != cudaSuccess) return amgp_cuda_fail(es, "pcg sync", __FILE__, __LINE__);
+        if (spec) AMGP_TRY(next_direction());
+        AMGP_CUDA(cudaEventSynchronize(ev.e));
         if (hs[S_BRK] != 0.0) {
             AMGP_CUDA(cudaStreamSynchronize(st));
             return finish(it - 1, false, true);
@@ -323,7 +343,10 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
             AMGP_CUDA(cudaStreamSynchronize(st));
             return finish(it, true, false);
         }
+        if (!spec) AMGP_TRY(next_direction());
         pc++;
+        rel_prev2 = rel_prev;
+        rel_prev = relres;
     }
     AMGP_CUDA(cudaStreamSynchronize(st));
     return finish(itmax, false, false);

@@ -1,0 +1,98 @@
+// Row-parallel SELL-32 kernels with pluggable epilogues.
+//
+// Every hot kernel of the library is "y_i = sum_j a_ij v_j in stored order,
+// then an elementwise epilogue on row i".  Two schedules compute y_i with
+// the SAME operations in the SAME order (so results are bitwise identical):
+//
+//   k_thread_rows  one thread per row, slots loaded SM_U at a time -- for
+//                  short rows (fine levels: 4-7 nnz), where the grid holds
+//                  enough warps to cover memory latency.
+//   k_split_rows   one CTA per 32-row slice; its NW warps compute the slot
+//                  products a_ij*v_j in parallel (every load independent ->
+//                  deep memory-level parallelism) into shared memory, then
+//                  each row is summed sequentially from 0.0 by warp 0.  For
+//                  coarse AMG levels (tens to hundreds of nnz per row, few
+//                  rows), where thread-per-row is latency bound.
+// Padding slots contribute +0.0 in k_split_rows and are skipped in
+// k_thread_rows: the row sum is never -0.0 (it starts at +0.0 and
+// round-to-nearest never produces -0.0 from a non-negative-zero operand),
+// so adding +0.0 leaves it unchanged bit for bit.
+#pragma once
+
+#include "amgp_common.cuh"
+
+#define ROWS_BLOCK 256
+#define ROWS_SLICES (ROWS_BLOCK / 32)
+#define ROWS_U 8
+#define SPLIT_WARPS 16
+#define SPLIT_CHUNK 192  // slots staged per pass: 192 * 32 * 8 B = 48 KB
+
+template <class Epi>
+__global__ void __launch_bounds__(ROWS_BLOCK)
+k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
+    const int64_t s = (int64_t)blockIdx.x * ROWS_SLICES + (threadIdx.x >> 5);
+    const int lane = threadIdx.x & 31;
+    if (s >= A.nslices) return;
+    double y = 0.0;
+    if (Epi::kSpmv) y = sell_row_dot<ROWS_U>(A, s, lane, xg);
+    const int64_t row = s * 32 + lane;
+    if (row < A.nrows) epi(row, y);
+}
+
+template <class Epi>
+__global__ void __launch_bounds__(SPLIT_WARPS * 32)
+k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
+    __shared__ double prod[SPLIT_CHUNK * 32];
+    const int64_t s = blockIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int64_t base = A.slice_ptr[s];
+    const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
+    const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
+    double sum = 0.0;
+    for (int j0 = 0; j0 < w; j0 += SPLIT_CHUNK) {
+        const int jn = min(SPLIT_CHUNK, w - j0);
+        for (int j = warp; j < jn; j += SPLIT_WARPS * 4) {
+            int32_t cc[4];
+            double vv[4];
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int jj = j + u * SPLIT_WARPS;
+                const bool ok = jj < jn;
+                const int64_t o = base + (int64_t)(j0 + jj) * 32 + lane;
+                cc[u] = ok ? ld_stream_s32(A.col + o, pf) : -1;
+                vv[u] = ok ? ld_stream_f64(A.val + o, pf) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; u++) {
+                const int jj = j + u * SPLIT_WARPS;
+                if (jj < jn)
+                    prod[jj * 32 + lane] = cc[u] >= 0 ? __dmul_rn(vv[u], ld_gather_f64(xg + cc[u], pl)) : 0.0;
+            }
+        }
+        __syncthreads();
+        if (warp == 0)
+            for (int j = 0; j < jn; j++) sum = __dadd_rn(sum, prod[j * 32 + lane]);
+        __syncthreads();
+    }
+    if (warp == 0) {
+        const int64_t row = s * 32 + lane;
+        if (row < A.nrows) epi(row, sum);
+    }
+}
+
+// Schedule choice: split when rows are long and there are too few slices to
+// keep the GPU's warps busy with thread-per-row.
+inline bool use_split(const amgp_mat *A) {
+    return A->max_width >= 24 && A->nslices < 148 * 64;
+}
+
+template <class Epi>
+int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &epi) {
+    if (A->nslices == 0) return AMGP_OK;
+    if (Epi::kSpmv && use_split(A))
+        k_split_rows<Epi><<<(unsigned)A->nslices, SPLIT_WARPS * 32, 0, ctx->stream>>>(view_of(A), xg, epi);
+    else
+        k_thread_rows<Epi><<<grid_for(A->nslices, ROWS_SLICES), ROWS_BLOCK, 0, ctx->stream>>>(view_of(A), xg, epi);
+    AMGP_CHECK_LAUNCH(ctx);
+    return AMGP_OK;
+}

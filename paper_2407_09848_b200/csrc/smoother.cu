@@ -1,11 +1,13 @@
 // K1/K2: the fused polynomial-smoother step kernels and smoother_apply.
 //
 // One kernel launch per degree step.  Each launch streams the matrix once
-// (SELL-32, thread per row) and fuses the SpMV of the step's operand with the
-// l1 scaling and the recurrence update of r / z|d / x -- the reference's k
-// SpMVs plus 2-4 numpy passes per step (smoothers.py:106-137) become k
-// passes over HBM.  The operand is double-buffered: rows gather the previous
-// step's operand while the new one is written to the other buffer.
+// (SELL-32) and fuses the SpMV of the step's operand with the l1 scaling and
+// the recurrence update of r / z|d / x -- the reference's k SpMVs plus 2-4
+// numpy passes per step (smoothers.py:106-137) become k passes over HBM.
+// The operand is double-buffered: rows gather the previous step's operand
+// while the new one is written to the other buffer.  The row schedule
+// (thread-per-row or split-slice, rows.cuh) is picked per matrix; both give
+// identical bits.
 //
 // Per-element arithmetic, every operation a
 // separate round-to-nearest binary64 op in the reference's order:
@@ -17,83 +19,76 @@
 // With x0 == 0 the first SpMV is skipped (b - A*0 == b bitwise).
 #include <algorithm>
 
-#include "amgp_common.cuh"
+#include "rows.cuh"
 
-#define SM_BLOCK 256
-#define SM_SLICES (SM_BLOCK / 32)
-#define SM_U 8
-
-// ---------------------------------------------------------------- kernels
+// ---------------------------------------------------------------- epilogues
 template <bool FIRST, bool LAST, bool X0>
-__global__ void __launch_bounds__(SM_BLOCK)
-k_cheb4_step(SellView A, const double *__restrict__ m, const double *__restrict__ b,
-             const double *__restrict__ xg, double *__restrict__ r, double *__restrict__ znew,
-             double *__restrict__ x, double cz, double cr, double beta) {
-    const int64_t s = (int64_t)blockIdx.x * SM_SLICES + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (s >= A.nslices) return;
-    double y = 0.0;
-    if (!FIRST || X0) y = sell_row_dot<SM_U>(A, s, lane, xg);
-    const int64_t row = s * 32 + lane;
-    if (row >= A.nrows) return;
-    const double rr = __dsub_rn(FIRST ? b[row] : r[row], y);
-    double z = FIRST ? __dmul_rn(0.0, cz) : __dmul_rn(xg[row], cz);
-    z = __dadd_rn(z, __dmul_rn(cr, __ddiv_rn(rr, m[row])));
-    const double xo = FIRST ? (X0 ? xg[row] : 0.0) : x[row];
-    x[row] = __dadd_rn(xo, __dmul_rn(beta, z));
-    if (!LAST) {
-        r[row] = rr;
-        znew[row] = z;
+struct Cheb4Step {
+    static constexpr bool kSpmv = !FIRST || X0;
+    const double *__restrict__ m;
+    const double *__restrict__ b;
+    const double *__restrict__ xg;  // x0 (first step) or z_{j-1}
+    double *__restrict__ r;
+    double *__restrict__ znew;
+    double *__restrict__ x;
+    double cz, cr, beta;
+    __device__ __forceinline__ void operator()(int64_t row, double y) const {
+        const double rr = __dsub_rn(FIRST ? b[row] : r[row], y);
+        double z = FIRST ? __dmul_rn(0.0, cz) : __dmul_rn(xg[row], cz);
+        z = __dadd_rn(z, __dmul_rn(cr, __ddiv_rn(rr, m[row])));
+        const double xo = FIRST ? (X0 ? xg[row] : 0.0) : x[row];
+        x[row] = __dadd_rn(xo, __dmul_rn(beta, z));
+        if (!LAST) {
+            r[row] = rr;
+            znew[row] = z;
+        }
     }
-}
+};
 
 template <bool FIRST, bool LAST, bool X0, bool RHO1>
-__global__ void __launch_bounds__(SM_BLOCK)
-k_cheb1_step(SellView A, const double *__restrict__ m, const double *__restrict__ b,
-             const double *__restrict__ xg, double *__restrict__ r, double *__restrict__ dnew,
-             double *__restrict__ x, double c0, double c1, double rho) {
-    // FIRST: c0 = theta ; else c0 = rho_j*rho_{j-1}, c1 = 2 rho_j / delta
-    const int64_t s = (int64_t)blockIdx.x * SM_SLICES + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (s >= A.nslices) return;
-    double y = 0.0;
-    if (!FIRST || X0) y = sell_row_dot<SM_U>(A, s, lane, xg);
-    const int64_t row = s * 32 + lane;
-    if (row >= A.nrows) return;
-    double rr, d, xo;
-    if (FIRST) {
-        rr = __ddiv_rn(__dsub_rn(b[row], y), m[row]);
-        if (!RHO1) rr = __ddiv_rn(rr, rho);
-        d = __ddiv_rn(rr, c0);
-        xo = X0 ? xg[row] : 0.0;
-    } else {
-        double sv = __ddiv_rn(y, m[row]);
-        if (!RHO1) sv = __ddiv_rn(sv, rho);
-        rr = __dsub_rn(r[row], sv);
-        d = __dadd_rn(__dmul_rn(xg[row], c0), __dmul_rn(c1, rr));
-        xo = x[row];
+struct Cheb1Step {
+    static constexpr bool kSpmv = !FIRST || X0;
+    const double *__restrict__ m;
+    const double *__restrict__ b;
+    const double *__restrict__ xg;  // x0 (init) or d_{j-1}
+    double *__restrict__ r;
+    double *__restrict__ dnew;
+    double *__restrict__ x;
+    double c0, c1, rho;  // init: c0 = theta; step: c0 = rho_j rho_{j-1}, c1 = 2 rho_j / delta
+    __device__ __forceinline__ void operator()(int64_t row, double y) const {
+        double rr, d, xo;
+        if (FIRST) {
+            rr = __ddiv_rn(__dsub_rn(b[row], y), m[row]);
+            if (!RHO1) rr = __ddiv_rn(rr, rho);
+            d = __ddiv_rn(rr, c0);
+            xo = X0 ? xg[row] : 0.0;
+        } else {
+            double sv = __ddiv_rn(y, m[row]);
+            if (!RHO1) sv = __ddiv_rn(sv, rho);
+            rr = __dsub_rn(r[row], sv);
+            d = __dadd_rn(__dmul_rn(xg[row], c0), __dmul_rn(c1, rr));
+            xo = x[row];
+        }
+        x[row] = __dadd_rn(xo, d);
+        if (!LAST) {
+            r[row] = rr;
+            dnew[row] = d;
+        }
     }
-    x[row] = __dadd_rn(xo, d);
-    if (!LAST) {
-        r[row] = rr;
-        dnew[row] = d;
-    }
-}
+};
 
 template <bool X0>
-__global__ void __launch_bounds__(SM_BLOCK)
-k_l1_sweep(SellView A, const double *__restrict__ m, const double *__restrict__ b,
-           const double *__restrict__ xin, double *__restrict__ xout) {
-    const int64_t s = (int64_t)blockIdx.x * SM_SLICES + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (s >= A.nslices) return;
-    double y = 0.0;
-    if (X0) y = sell_row_dot<SM_U>(A, s, lane, xin);
-    const int64_t row = s * 32 + lane;
-    if (row >= A.nrows) return;
-    const double rr = __dsub_rn(b[row], y);
-    xout[row] = __dadd_rn(X0 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
-}
+struct L1Sweep {
+    static constexpr bool kSpmv = X0;
+    const double *__restrict__ m;
+    const double *__restrict__ b;
+    const double *__restrict__ xin;
+    double *__restrict__ xout;
+    __device__ __forceinline__ void operator()(int64_t row, double y) const {
+        const double rr = __dsub_rn(b[row], y);
+        xout[row] = __dadd_rn(X0 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
+    }
+};
 
 // sparse.py:128-139 fused_update (elementwise, in place)
 __global__ void k_fused_update(int64_t n, double rp, double c, const double *__restrict__ s,
@@ -111,8 +106,7 @@ __global__ void k_fused_update(int64_t n, double rp, double c, const double *__r
 
 // ---------------------------------------------------------------- host side
 // smoothers.py:112-135 scalars, evaluated as Python evaluates them (binary64,
-// left-to-right; host code is compiled with -ffp-contract=off semantics since
-// every operation is a separate statement on doubles).
+// one operation per statement; built with -ffp-contract=off).
 int make_smoother_plan(const amgp_smoother_cfg *cfg, SmootherPlan *plan) {
     if (!cfg) return amgp_fail(AMGP_EINVAL, "null smoother config");
     if (cfg->family < AMGP_L1_JACOBI || cfg->family > AMGP_OPT_CHEB1)
@@ -139,8 +133,7 @@ int make_smoother_plan(const amgp_smoother_cfg *cfg, SmootherPlan *plan) {
         }
     } else if (cfg->family == AMGP_OPT_CHEB1) {
         if (!(cfg->a > 0.0 && cfg->a < 1.0)) return amgp_fail(AMGP_EINVAL, "a must lie in (0, 1)");
-        // chebyshev.py:82-83
-        double theta = (1.0 + cfg->a) / 2.0;
+        double theta = (1.0 + cfg->a) / 2.0;  // chebyshev.py:82-83
         double delta = (1.0 - cfg->a) / 2.0;
         double sigma1 = theta / delta;
         plan->coef[0] = theta;
@@ -167,33 +160,29 @@ extern "C" int amgp_smoother_coefficients(const amgp_smoother_cfg *cfg, double *
 }
 
 template <bool FIRST, bool LAST>
-static void launch_cheb4(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
-                         const double *xg, bool x0, double *r, double *znew, double *x,
-                         double cz, double cr, double beta) {
-    const unsigned g = grid_for(A->nslices, SM_SLICES);
+static int launch_cheb4(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
+                        const double *xg, bool x0, double *r, double *znew, double *x, double cz,
+                        double cr, double beta) {
     if (FIRST && x0)
-        k_cheb4_step<FIRST, LAST, true><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, znew, x, cz, cr, beta);
-    else
-        k_cheb4_step<FIRST, LAST, false><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, znew, x, cz, cr, beta);
+        return launch_rows(ctx, A, xg, Cheb4Step<FIRST, LAST, true>{m, b, xg, r, znew, x, cz, cr, beta});
+    return launch_rows(ctx, A, xg, Cheb4Step<FIRST, LAST, false>{m, b, xg, r, znew, x, cz, cr, beta});
 }
 
 template <bool FIRST, bool LAST, bool X0>
-static void launch_cheb1_x0(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
-                            const double *xg, double *r, double *dnew, double *x, double c0,
-                            double c1, double rho) {
-    const unsigned g = grid_for(A->nslices, SM_SLICES);
+static int launch_cheb1_x0(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
+                           const double *xg, double *r, double *dnew, double *x, double c0,
+                           double c1, double rho) {
     if (rho == 1.0)
-        k_cheb1_step<FIRST, LAST, X0, true><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, dnew, x, c0, c1, rho);
-    else
-        k_cheb1_step<FIRST, LAST, X0, false><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xg, r, dnew, x, c0, c1, rho);
+        return launch_rows(ctx, A, xg, Cheb1Step<FIRST, LAST, X0, true>{m, b, xg, r, dnew, x, c0, c1, rho});
+    return launch_rows(ctx, A, xg, Cheb1Step<FIRST, LAST, X0, false>{m, b, xg, r, dnew, x, c0, c1, rho});
 }
 
 template <bool FIRST, bool LAST>
-static void launch_cheb1(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
-                         const double *xg, bool x0, double *r, double *dnew, double *x,
-                         double c0, double c1, double rho) {
-    if (FIRST && x0) launch_cheb1_x0<FIRST, LAST, true>(ctx, A, m, b, xg, r, dnew, x, c0, c1, rho);
-    else launch_cheb1_x0<FIRST, LAST, false>(ctx, A, m, b, xg, r, dnew, x, c0, c1, rho);
+static int launch_cheb1(amgp_ctx *ctx, const amgp_mat *A, const double *m, const double *b,
+                        const double *xg, bool x0, double *r, double *dnew, double *x, double c0,
+                        double c1, double rho) {
+    if (FIRST && x0) return launch_cheb1_x0<FIRST, LAST, true>(ctx, A, m, b, xg, r, dnew, x, c0, c1, rho);
+    return launch_cheb1_x0<FIRST, LAST, false>(ctx, A, m, b, xg, r, dnew, x, c0, c1, rho);
 }
 
 int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const SmootherPlan &p,
@@ -208,12 +197,8 @@ int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const Sm
         const double *xin = x0;
         for (int s = 1; s <= k; s++) {
             double *xout = ((k - s) % 2 == 0) ? x : tmp;
-            const unsigned g = grid_for(A->nslices, SM_SLICES);
-            if (s == 1 && !hx0)
-                k_l1_sweep<false><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, nullptr, xout);
-            else
-                k_l1_sweep<true><<<g, SM_BLOCK, 0, ctx->stream>>>(view_of(A), m, b, xin, xout);
-            AMGP_CHECK_LAUNCH(ctx);
+            if (s == 1 && !hx0) AMGP_TRY(launch_rows(ctx, A, nullptr, L1Sweep<false>{m, b, nullptr, xout}));
+            else AMGP_TRY(launch_rows(ctx, A, xin, L1Sweep<true>{m, b, xin, xout}));
             xin = xout;
         }
         return AMGP_OK;
@@ -224,11 +209,10 @@ int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const Sm
                          be = p.coef[3 * (j - 1) + 2];
             const double *xg = (j == 1) ? x0 : buf[(j - 1) & 1];
             double *zn = buf[j & 1];
-            if (j == 1 && k == 1) launch_cheb4<true, true>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
-            else if (j == 1) launch_cheb4<true, false>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
-            else if (j == k) launch_cheb4<false, true>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
-            else launch_cheb4<false, false>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be);
-            AMGP_CHECK_LAUNCH(ctx);
+            if (j == 1 && k == 1) AMGP_TRY((launch_cheb4<true, true>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be)));
+            else if (j == 1) AMGP_TRY((launch_cheb4<true, false>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be)));
+            else if (j == k) AMGP_TRY((launch_cheb4<false, true>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be)));
+            else AMGP_TRY((launch_cheb4<false, false>(ctx, A, m, b, xg, hx0, r, zn, x, cz, cr, be)));
         }
         return AMGP_OK;
     }
@@ -239,14 +223,13 @@ int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const Sm
         const bool last = (j == k - 1);
         if (j == 0) {
             const double theta = p.coef[0];
-            if (last) launch_cheb1<true, true>(ctx, A, m, b, xg, hx0, r, dn, x, theta, 0.0, p.rho);
-            else launch_cheb1<true, false>(ctx, A, m, b, xg, hx0, r, dn, x, theta, 0.0, p.rho);
+            if (last) AMGP_TRY((launch_cheb1<true, true>(ctx, A, m, b, xg, hx0, r, dn, x, theta, 0.0, p.rho)));
+            else AMGP_TRY((launch_cheb1<true, false>(ctx, A, m, b, xg, hx0, r, dn, x, theta, 0.0, p.rho)));
         } else {
             const double rp = p.coef[1 + 2 * (j - 1)], c = p.coef[2 + 2 * (j - 1)];
-            if (last) launch_cheb1<false, true>(ctx, A, m, b, xg, hx0, r, dn, x, rp, c, p.rho);
-            else launch_cheb1<false, false>(ctx, A, m, b, xg, hx0, r, dn, x, rp, c, p.rho);
+            if (last) AMGP_TRY((launch_cheb1<false, true>(ctx, A, m, b, xg, hx0, r, dn, x, rp, c, p.rho)));
+            else AMGP_TRY((launch_cheb1<false, false>(ctx, A, m, b, xg, hx0, r, dn, x, rp, c, p.rho)));
         }
-        AMGP_CHECK_LAUNCH(ctx);
     }
     return AMGP_OK;
 }

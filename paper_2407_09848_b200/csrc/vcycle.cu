@@ -56,11 +56,15 @@ k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__
             if (s > 1) {
                 const int64_t sl = row >> 5;
                 const int lane = row & 31;
-                const int64_t base = A.slice_ptr[sl];
-                const int w = (int)((A.slice_ptr[sl + 1] - base) >> 5);
+                const int64_t base = __ldg(A.slice_ptr + sl);
+                const int w = (int)((__ldg(A.slice_ptr + sl + 1) - base) >> 5);
+                const int32_t *cp = A.col + base + lane;
+                const double *vp = A.val + base + lane;
+#pragma unroll 8
                 for (int j = 0; j < w; j++) {
-                    const int32_t c = A.col[base + (int64_t)j * 32 + lane];
-                    if (c >= 0) y = __dadd_rn(y, __dmul_rn(A.val[base + (int64_t)j * 32 + lane], xin[c]));
+                    const int32_t c = __ldg(cp + (int64_t)j * 32);
+                    const double p = c >= 0 ? __dmul_rn(__ldg(vp + (int64_t)j * 32), xin[c]) : 0.0;
+                    y = __dadd_rn(y, p);  // padding adds +0.0: bitwise neutral (rows.cuh)
                 }
             }
             const double rr = __dsub_rn(b[row], y);

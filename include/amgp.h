@@ -182,6 +182,9 @@ int amgp_setup_smooth_prolongator(int64_t n, const int64_t *row_ptr, const int64
 int amgp_setup_galerkin(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
                         const double *values, int64_t nc, const int64_t *p_row_ptr,
                         const int64_t *p_col_idx, const double *p_values, amgp_hcsr **Ac);
+/* numpy float64 dot (x @ y) exactly as OpenBLAS 0.3.30's SkylakeX ddot with
+ * `threads` BLAS threads evaluates it (amg.py:211-212 power iteration). */
+double amgp_setup_blas_dot(int64_t n, const double *x, const double *y, int threads);
 /* host y = A x in stored order (the power iteration of amg.py:194-216) */
 int amgp_setup_spmv(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
                     const double *values, const double *x, double *y);

@@ -101,6 +101,7 @@ _SIGS = {
     "amgp_setup_galerkin": (C.c_int, [C.c_int64, _P64, _P64, _PD, C.c_int64, _P64, _P64, _PD,
                                        C.POINTER(_VP)]),
     "amgp_setup_spmv": (C.c_int, [C.c_int64, _P64, _P64, _PD, _PD, _PD]),
+    "amgp_setup_blas_dot": (C.c_double, [C.c_int64, _PD, _PD, C.c_int]),
 }
 
 _lib = None

@@ -532,6 +532,72 @@ int amgp_setup_galerkin(int64_t n, const int64_t *rp, const int64_t *ci, const d
     return AMGP_OK;
 }
 
+// numpy's float64 dot (v @ w, np.linalg.norm) as the reference executes it:
+// OpenBLAS 0.3.30 ddot, SkylakeX kernel (the kernel numpy's bundled
+// scipy-openblas dispatches on AVX-512 hosts).  n1 = n & -16 elements go
+// through the micro-kernel: four 8-wide FMA accumulators over 32-element
+// blocks, folded to four 4-wide ones, 16-element blocks on the four 4-wide
+// accumulators, then ((a0+a1)+a2)+a3, 256->128 fold and a horizontal add
+// (verified bit-exact against numpy for 1, 3 and 8 BLAS threads); the rest is
+// dot = fma(y, x, dot).  With `threads` > 1 and n > 10000, OpenBLAS splits n
+// into contiguous chunks (width = ceil(remaining / threads_left)) and sums
+// the per-chunk dots in order from 0.0.  The reference's hierarchy therefore
+// depends on the host's OpenBLAS thread count; the canonical choice here is
+// one thread (SURVEY.md section 8d runs the reference with
+// OPENBLAS_NUM_THREADS=1).
+static double ddot_chunk(int64_t n, const double *x, const double *y) {
+    double dot = 0.0;
+    const int64_t n1 = n & -16;
+    if (n1) {
+        double a05[8] = {0}, a15[8] = {0}, a25[8] = {0}, a35[8] = {0};
+        const int64_t n32 = n1 & ~(int64_t)31;
+        int64_t i = 0;
+        for (; i < n32; i += 32)
+            for (int l = 0; l < 8; l++) {
+                a05[l] = fma(x[i + l], y[i + l], a05[l]);
+                a15[l] = fma(x[i + 8 + l], y[i + 8 + l], a15[l]);
+                a25[l] = fma(x[i + 16 + l], y[i + 16 + l], a25[l]);
+                a35[l] = fma(x[i + 24 + l], y[i + 24 + l], a35[l]);
+            }
+        double a0[4], a1[4], a2[4], a3[4];
+        for (int l = 0; l < 4; l++) {
+            a0[l] = a05[l] + a05[l + 4];
+            a1[l] = a15[l] + a15[l + 4];
+            a2[l] = a25[l] + a25[l + 4];
+            a3[l] = a35[l] + a35[l + 4];
+        }
+        for (; i < n1; i += 16)
+            for (int l = 0; l < 4; l++) {
+                a0[l] = fma(x[i + l], y[i + l], a0[l]);
+                a1[l] = fma(x[i + 4 + l], y[i + 4 + l], a1[l]);
+                a2[l] = fma(x[i + 8 + l], y[i + 8 + l], a2[l]);
+                a3[l] = fma(x[i + 12 + l], y[i + 12 + l], a3[l]);
+            }
+        double s[4];
+        for (int l = 0; l < 4; l++) s[l] = ((a0[l] + a1[l]) + a2[l]) + a3[l];
+        const double h0 = s[0] + s[2], h1 = s[1] + s[3];
+        dot = h0 + h1;
+    }
+    for (int64_t i = n1; i < n; i++) dot = fma(y[i], x[i], dot);
+    return dot;
+}
+
+extern "C" double amgp_setup_blas_dot(int64_t n, const double *x, const double *y, int threads) {
+    if (n <= 0) return 0.0;
+    if (threads <= 1 || n <= 10000) return ddot_chunk(n, x, y);
+    double dot = 0.0;
+    int64_t i = n, start = 0;
+    for (int t = 0; i > 0; t++) {
+        const int64_t left = threads - t;
+        int64_t width = (i + left - 1) / left;
+        i -= width;
+        if (i < 0) width += i;
+        dot = dot + ddot_chunk(width, x + start, y + start);
+        start += width;
+    }
+    return dot;
+}
+
 // In-order host SpMV (scipy csr_matvec order), row blocks on threads.
 int amgp_setup_spmv(int64_t n, const int64_t *rp, const int64_t *ci, const double *v,
                     const double *x, double *y) {

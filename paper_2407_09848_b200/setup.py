@@ -85,8 +85,27 @@ def host_spmv(A, x):
     return y
 
 
+def blas_threads():
+    """OpenBLAS thread count whose ddot order the setup reproduces
+    (AMGP_BLAS_THREADS, default 1 -- the reference run single-threaded)."""
+    return int(os.environ.get("AMGP_BLAS_THREADS", "1"))
+
+
+def blas_dot(x, y, threads=None):
+    """numpy's float64 dot as OpenBLAS (SkylakeX kernel) evaluates it, host-independent."""
+    x = np.ascontiguousarray(x, dtype=np.float64)
+    y = np.ascontiguousarray(y, dtype=np.float64)
+    return N.lib().amgp_setup_blas_dot(len(x), x.ctypes.data_as(N._PD), y.ctypes.data_as(N._PD),
+                                       int(blas_threads() if threads is None else threads))
+
+
 def estimate_lambda_max(A, d, iters=25):
-    """Power iteration on D^-1/2 A D^-1/2 (amg.py:194-216), same seeded start."""
+    """Power iteration on D^-1/2 A D^-1/2 (amg.py:194-216), same seeded start.
+
+    The dots and the norm use blas_dot: the reference takes them through
+    numpy -> OpenBLAS ddot, whose summation order (SIMD accumulators, thread
+    split) decides the last bits of lambda and hence of every coarse level.
+    """
     if np.any(d <= 0.0):
         raise ValueError("diagonal must be positive")
     _threads()
@@ -95,8 +114,8 @@ def estimate_lambda_max(A, d, iters=25):
     lam = 1.0
     for _ in range(iters):
         w = host_spmv(A, v / ds) / ds
-        lam = float(v @ w) / float(v @ v)
-        nrm = np.linalg.norm(w)
+        lam = blas_dot(v, w) / blas_dot(v, v)
+        nrm = np.sqrt(blas_dot(w, w))
         if nrm == 0.0:
             return 0.0
         v = w / nrm

@@ -22,15 +22,24 @@ It imports ``amgpoly`` from /root/reference/pkg/src and writes
   iteration tables (rtol 1e-6) at 32^3.
 
 Digests are over little-endian bytes of int64 (indices) / float64 (values).
+
+The reference runs with OPENBLAS_NUM_THREADS=1 (set below): its lambda_max
+power iteration takes dot products through OpenBLAS, whose thread split
+changes the last bits of lambda (and thus every coarse level) with the core
+count.  One BLAS thread is the convention of SURVEY.md section 8d.
 """
 
 from __future__ import annotations
 
-import hashlib
-import json
 import os
-import sys
-import time
+
+os.environ["OPENBLAS_NUM_THREADS"] = "1"
+os.environ["OMP_NUM_THREADS"] = "1"
+
+import hashlib  # noqa: E402
+import json  # noqa: E402
+import sys  # noqa: E402
+import time  # noqa: E402
 
 import numpy as np
 

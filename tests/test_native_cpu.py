@@ -22,7 +22,7 @@ from paper_2407_09848_b200 import _native as N
 
 def header_symbols():
     text = open(os.path.join(REPO, "include", "amgp.h")).read()
-    decl = r"^\s*(?:int|const char \*)\s*(amgp_[a-z0-9_]+)\s*\("
+    decl = r"^\s*(?:int|double|const char \*)\s*(amgp_[a-z0-9_]+)\s*\("
     return sorted(set(re.findall(decl, text, flags=re.M)))
 
 

@@ -102,6 +102,24 @@ def test_lambda_and_smoothing_unit_cases():
     assert abs(lam - exact) <= 0.05 * exact
 
 
+@pytest.mark.parametrize("threads", [1, 3, 8])
+def test_blas_dot_emulation_matches_numpy(threads):
+    """amgp_setup_blas_dot reproduces numpy's OpenBLAS ddot bit for bit
+    (only checkable on a host whose OpenBLAS dispatches the SkylakeX kernel)."""
+    from threadpoolctl import threadpool_info, threadpool_limits
+
+    arch = [i.get("architecture") for i in threadpool_info() if i.get("internal_api") == "openblas"]
+    if "SkylakeX" not in arch:
+        pytest.skip(f"host OpenBLAS kernel {arch} is not SkylakeX")
+    rng = np.random.default_rng(threads)
+    with threadpool_limits(threads, user_api="blas"):
+        for n in [1, 15, 16, 17, 32, 48, 100, 9999, 10001, 65535, 262144, 300001]:
+            x = rng.standard_normal(n) * 10 ** rng.uniform(-3, 3, n)
+            y = rng.standard_normal(n)
+            assert S.blas_dot(x, y, threads) == x @ y, n
+            assert np.sqrt(S.blas_dot(y, y, threads)) == np.linalg.norm(y), n
+
+
 def test_operator_complexity_and_summary():
     A, _ = P.poisson3d(8)
     h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind="pairwise_matching"))

@@ -37,35 +37,52 @@ struct amgp_hier {
     std::mutex mu;
 };
 
-#define COARSE_SMEM_MAX_ROWS 6144  // 2 x 6144 doubles = 96 KB of shared memory
+#define COARSE_SMEM_BYTES (200 * 1024)
 
-// K6: all l1-Jacobi sweeps of the coarsest level in one CTA.  The iterate
-// ping-pongs between two shared-memory buffers; every row's arithmetic is the
-// k_l1_sweep arithmetic, so the result is bitwise the multi-launch result.
+static inline size_t coarse_smem(const amgp_mat *A) {
+    return 16 * (size_t)A->nrows + 20 * (size_t)A->stored + 64;
+}
+
+// K6: all l1-Jacobi sweeps of the coarsest level in one CTA.  The level's
+// SELL slots are staged in shared memory once; per sweep every (row, slot)
+// product is formed in parallel by all threads, then each row is summed in
+// slot order (padding contributes +0.0, bitwise neutral -- rows.cuh) and
+// updated as k_l1_sweep does, so the result is bitwise the multi-launch one.
 __global__ void __launch_bounds__(1024)
 k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__ b,
             double *__restrict__ x, int sweeps) {
-    extern __shared__ double sx[];
+    extern __shared__ double sh[];
     const int64_t n = A.nrows;
-    double *buf[2] = {sx, sx + n};
+    const int64_t stored = A.slice_ptr[A.nslices];
+    double *buf[2] = {sh, sh + n};
+    double *pv = sh + 2 * n;
+    double *prod = pv + stored;
+    int32_t *pc = (int32_t *)(prod + stored);
+    for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
+        pv[e] = A.val[e];
+        pc[e] = A.col[e];
+    }
+    __syncthreads();
     for (int s = 1; s <= sweeps; s++) {
         const double *xin = buf[(s - 1) & 1];
         double *xout = buf[s & 1];
+        if (s > 1) {
+            for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
+                const int32_t c = pc[e];
+                prod[e] = c >= 0 ? __dmul_rn(pv[e], xin[c]) : 0.0;
+            }
+            __syncthreads();
+        }
         for (int64_t row = threadIdx.x; row < n; row += blockDim.x) {
             double y = 0.0;
             if (s > 1) {
                 const int64_t sl = row >> 5;
                 const int lane = row & 31;
-                const int64_t base = __ldg(A.slice_ptr + sl);
-                const int w = (int)((__ldg(A.slice_ptr + sl + 1) - base) >> 5);
-                const int32_t *cp = A.col + base + lane;
-                const double *vp = A.val + base + lane;
+                const int64_t base = A.slice_ptr[sl];
+                const int w = (int)((A.slice_ptr[sl + 1] - base) >> 5);
+                const double *pp = prod + base + lane;
 #pragma unroll 8
-                for (int j = 0; j < w; j++) {
-                    const int32_t c = __ldg(cp + (int64_t)j * 32);
-                    const double p = c >= 0 ? __dmul_rn(__ldg(vp + (int64_t)j * 32), xin[c]) : 0.0;
-                    y = __dadd_rn(y, p);  // padding adds +0.0: bitwise neutral (rows.cuh)
-                }
+                for (int j = 0; j < w; j++) y = __dadd_rn(y, pp[j * 32]);
             }
             const double rr = __dsub_rn(b[row], y);
             xout[row] = __dadd_rn(s > 1 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
@@ -120,9 +137,8 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
     }
     if (h->coarse_solver == AMGP_COARSE_SMOOTHER)
         return smoother_enqueue(ctx, A, h->m[l], h->plan[l], r, nullptr, z, h->work[l]);
-    if (n <= COARSE_SMEM_MAX_ROWS) {
-        const size_t smem = 2 * n * sizeof(double);
-        k_coarse_l1<<<1, 1024, smem, ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
+    if (coarse_smem(A) <= COARSE_SMEM_BYTES) {
+        k_coarse_l1<<<1, 1024, coarse_smem(A), ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
@@ -242,7 +258,7 @@ extern "C" int amgp_hier_create(amgp_ctx *ctx, int nlevels, amgp_mat *const *A,
     }
     // K6 needs up to 96 KB of dynamic shared memory
     cudaFuncSetAttribute(k_coarse_l1, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         2 * COARSE_SMEM_MAX_ROWS * (int)sizeof(double));
+                         COARSE_SMEM_BYTES);
     cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     *out = h;
     return AMGP_OK;

@@ -145,6 +145,27 @@ int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const double *b, do
                    int x0_given, int variant, double tol, int itmax, double *history_host,
                    amgp_solve_report *report);
 
+/* ---- multi-GPU: one process per GPU, row-block partitions ---
+ * The reference is single-process; this is the paper's MPI+CUDA layer
+ * rebuilt on NCCL over NVLink.  NCCL is dlopen'ed. */
+/* 128-byte ncclUniqueId (rank 0 creates it and shares it out of band) */
+int amgp_comm_unique_id(char *id128);
+int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const char *id128);
+int amgp_ctx_comm_info(amgp_ctx *ctx, int *nranks, int *rank);
+/* Attach a halo plan: local columns [0, nown) index the rank's own operand
+ * entries, [nown, ncols) the halo, received per SpMV from `peers` (recv_cnt
+ * each, in peer order); this rank sends send_cnt[q] own entries
+ * (send_idx, concatenated in peer order) to peers[q].  Slices whose columns
+ * stay below nown run while the exchange is in flight. */
+int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const int *peers,
+                      const int64_t *send_cnt, const int64_t *send_idx, const int64_t *recv_cnt);
+int amgp_mat_halo_info(const amgp_mat *A, int64_t *nown, int64_t *nhalo, int64_t *n_interior,
+                       int64_t *n_boundary);
+/* Rewrite the global columns of a generated row block to local ones: owned
+ * [own_lo, own_hi) first, then halo segments [seg_lo[q], seg_hi[q]) in order. */
+int amgp_mat_localize(amgp_mat *A, int64_t own_lo, int64_t own_hi, int nseg,
+                      const int64_t *seg_lo, const int64_t *seg_hi);
+
 /* ---- host-side helpers (no device needed; used by CPU tests) ------------ */
 /* Pack a CSR into SELL-32 on the host.  Call with outputs NULL to get
  * *nslices and *stored; then with arrays slice_ptr[nslices+1], col[stored]

@@ -29,7 +29,7 @@ FLAGS = [
     "-Xptxas", "-warn-spills",
     "-I", os.path.join(REPO, "include"),
 ]
-LIBS = ["-lnccl"]
+LIBS = ["-ldl"]  # NCCL is dlopen'ed at run time (csrc/dist.cu)
 
 
 def sources():

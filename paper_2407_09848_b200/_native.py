@@ -102,6 +102,12 @@ _SIGS = {
                                        C.POINTER(_VP)]),
     "amgp_setup_spmv": (C.c_int, [C.c_int64, _P64, _P64, _PD, _PD, _PD]),
     "amgp_setup_blas_dot": (C.c_double, [C.c_int64, _PD, _PD, C.c_int]),
+    "amgp_comm_unique_id": (C.c_int, [C.c_char_p]),
+    "amgp_ctx_init_comm": (C.c_int, [_VP, C.c_int, C.c_int, C.c_char_p]),
+    "amgp_ctx_comm_info": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "amgp_mat_set_halo": (C.c_int, [_VP, C.c_int64, C.c_int, C.POINTER(C.c_int), _P64, _P64, _P64]),
+    "amgp_mat_halo_info": (C.c_int, [_VP, _P64, _P64, _P64, _P64]),
+    "amgp_mat_localize": (C.c_int, [_VP, C.c_int64, C.c_int64, C.c_int, _P64, _P64]),
 }
 
 _lib = None

@@ -47,6 +47,8 @@ int amgp_cuda_fail(cudaError_t e, const char *what, const char *file, int line);
     } while (0)
 
 // ---------------------------------------------------------------- objects
+struct NcclApi;  // dist.cu: NCCL entry points resolved with dlopen
+
 struct amgp_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -58,6 +60,28 @@ struct amgp_ctx {
     int64_t red_partial_n = 0;
     double *scalars = nullptr;       // device scalar block (see pcg.cu)
     double *host_scalars = nullptr;  // pinned mirror
+    // multi-GPU (dist.cu): one NCCL communicator per context, its stream and
+    // the events that fork/join halo exchanges with the compute stream
+    void *comm = nullptr;  // ncclComm_t
+    int nranks = 1, rank = 0;
+    cudaStream_t comm_stream = nullptr;
+    cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
+    double *gather_buf = nullptr;  // allgather scratch for global dots
+};
+
+// Halo plan of a row-distributed matrix (dist.cu).  Columns [0, nown) are
+// the rank's own entries of the operand vector; columns >= nown index the
+// halo buffer, filled per SpMV by NCCL send/recv with the neighbours.
+struct HaloPlan {
+    int64_t nown = 0, nhalo = 0, nsend = 0;
+    std::vector<int> peers;                       // neighbour ranks (ascending)
+    std::vector<int64_t> send_cnt, send_off;      // per peer, into sendbuf
+    std::vector<int64_t> recv_cnt, recv_off;      // per peer, into halo
+    int64_t *send_idx = nullptr;                  // device [nsend] own indices
+    double *sendbuf = nullptr;                    // device [nsend]
+    double *halo = nullptr;                       // device [nhalo]
+    int32_t *interior = nullptr, *boundary = nullptr;  // device slice lists
+    int64_t n_interior = 0, n_boundary = 0;
 };
 
 struct amgp_mat {
@@ -69,6 +93,8 @@ struct amgp_mat {
     double *val = nullptr;         // [stored]
     int32_t max_width = 0;
     int64_t row_offset = 0;  // first global row of a generated row block
+    std::vector<int64_t> slice_maxcol;  // host: largest column per slice (-1: empty)
+    HaloPlan *halo = nullptr;           // non-null: distributed operand
     // per-matrix smoother workspace (r, two operand buffers, x copy)
     double *work = nullptr;
     int64_t work_n = 0;
@@ -82,11 +108,23 @@ struct SellView {
     const double *__restrict__ val;
     int64_t nrows;
     int64_t nslices;
+    const int32_t *__restrict__ slist;  // slices to process (nullptr: 0..nlist-1)
+    int64_t nlist;
+    int64_t nown;                       // gathers of columns >= nown read xh
+    const double *__restrict__ xh;
 };
 
 inline SellView view_of(const amgp_mat *A) {
-    return SellView{A->slice_ptr, A->col, A->val, A->nrows, A->nslices};
+    return SellView{A->slice_ptr, A->col, A->val, A->nrows, A->nslices,
+                    nullptr,      A->nslices, INT64_MAX, nullptr};
 }
+
+// Exchange the halo of operand x (own part) for a distributed matrix; after
+// it, kernels may gather x through view.xh (dist.cu).
+int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x);
+int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A);
+void mat_free_halo(amgp_mat *A);
+int refresh_slice_maxcol(amgp_mat *A);  // recompute A->slice_maxcol from the device columns
 
 // Resolved smoother configuration with host-computed step scalars
 // (smoothers.py:112-135 expressions evaluated in binary64 on the host).
@@ -174,7 +212,10 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
             vv[u] = ok ? ld_stream_f64(v + (int64_t)(j + u) * AMGP_SLICE, pf) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < U; u++) xx[u] = cc[u] >= 0 ? ld_gather_f64(x + cc[u], pl) : 0.0;
+        for (int u = 0; u < U; u++)
+            xx[u] = cc[u] < 0 ? 0.0
+                              : (cc[u] < A.nown ? ld_gather_f64(x + cc[u], pl)
+                                                : ld_gather_f64(A.xh + (cc[u] - A.nown), pl));
 #pragma unroll
         for (int u = 0; u < U; u++)
             if (cc[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(vv[u], xx[u]));

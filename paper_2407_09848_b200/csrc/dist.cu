@@ -1,0 +1,340 @@
+// Multi-GPU plumbing: one process per GPU, row-block partitions, NCCL halo
+// exchange overlapped with the interior rows.
+//
+// NCCL is resolved at run time with dlopen("libnccl.so.2"), so the library
+// shares whatever NCCL the process already loaded (torch's when
+// torch.distributed is in use) instead of pinning its own copy.
+//
+// A distributed matrix keeps global row order inside the rank's block and
+// local column indices: [0, nown) = the rank's own operand entries,
+// [nown, nown + nhalo) = the halo buffer, filled by one grouped
+// ncclSend/ncclRecv per SpMV.  Row arithmetic does not change with the
+// partition, so every kernel returns the single-GPU bits.
+#include <dlfcn.h>
+#include <nccl.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <vector>
+
+#include "amgp_common.cuh"
+
+struct NcclApi {
+    bool ok = false;
+    ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
+    ncclResult_t (*CommInitRank)(ncclComm_t *, int, ncclUniqueId, int) = nullptr;
+    ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+    ncclResult_t (*Send)(const void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*Recv)(void *, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+    ncclResult_t (*GroupStart)() = nullptr;
+    ncclResult_t (*GroupEnd)() = nullptr;
+    ncclResult_t (*AllGather)(const void *, void *, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+    const char *(*GetErrorString)(ncclResult_t) = nullptr;
+};
+
+static NcclApi *nccl() {
+    static NcclApi api;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+        if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+        if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+        if (h) {
+#define SYM(f) api.f = (decltype(api.f))dlsym(h, "nccl" #f)
+            SYM(GetUniqueId);
+            SYM(CommInitRank);
+            SYM(CommDestroy);
+            SYM(Send);
+            SYM(Recv);
+            SYM(GroupStart);
+            SYM(GroupEnd);
+            SYM(AllGather);
+            SYM(GetErrorString);
+#undef SYM
+            api.ok = api.GetUniqueId && api.CommInitRank && api.Send && api.Recv && api.GroupStart &&
+                     api.GroupEnd && api.AllGather;
+        }
+    }
+    return api.ok ? &api : nullptr;
+}
+
+#define NCCL_TRY(call)                                                                   \
+    do {                                                                                 \
+        ncclResult_t _r = (call);                                                        \
+        if (_r != ncclSuccess)                                                           \
+            return amgp_fail(AMGP_ENCCL, std::string("NCCL error in " #call ": ") +      \
+                                             (nccl()->GetErrorString ? nccl()->GetErrorString(_r) : "?")); \
+    } while (0)
+
+extern "C" int amgp_comm_unique_id(char *out) {
+    NcclApi *api = nccl();
+    if (!api) return amgp_fail(AMGP_ENCCL, "libnccl.so.2 not found");
+    if (!out) return amgp_fail(AMGP_EINVAL, "null output");
+    ncclUniqueId id;
+    NCCL_TRY(api->GetUniqueId(&id));
+    memcpy(out, id.internal, NCCL_UNIQUE_ID_BYTES);
+    return AMGP_OK;
+}
+
+extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const char *id) {
+    if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks)
+        return amgp_fail(AMGP_EINVAL, "amgp_ctx_init_comm: bad argument");
+    NcclApi *api = nccl();
+    if (!api) return amgp_fail(AMGP_ENCCL, "libnccl.so.2 not found");
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    ncclUniqueId uid;
+    memcpy(uid.internal, id, NCCL_UNIQUE_ID_BYTES);
+    ncclComm_t comm;
+    NCCL_TRY(api->CommInitRank(&comm, nranks, uid, rank));
+    ctx->comm = comm;
+    ctx->nranks = nranks;
+    ctx->rank = rank;
+    AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
+    AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_exchanged, cudaEventDisableTiming));
+    AMGP_CUDA(cudaMalloc(&ctx->gather_buf, (size_t)nranks * 16 * sizeof(double)));
+    return AMGP_OK;
+}
+
+extern "C" int amgp_ctx_comm_info(amgp_ctx *ctx, int *nranks, int *rank) {
+    if (!ctx) return amgp_fail(AMGP_EINVAL, "null context");
+    if (nranks) *nranks = ctx->nranks;
+    if (rank) *rank = ctx->rank;
+    return AMGP_OK;
+}
+
+// ---------------------------------------------------------------- halo plans
+static void halo_free(HaloPlan *h) {
+    if (!h) return;
+    cudaFree(h->send_idx);
+    cudaFree(h->sendbuf);
+    cudaFree(h->halo);
+    cudaFree(h->interior);
+    cudaFree(h->boundary);
+    delete h;
+}
+
+void mat_free_halo(amgp_mat *A) {
+    halo_free(A->halo);
+    A->halo = nullptr;
+}
+
+extern "C" int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const int *peers,
+                                 const int64_t *send_cnt, const int64_t *send_idx,
+                                 const int64_t *recv_cnt) {
+    if (!A || nown < 0 || npeers < 0 || (npeers && (!peers || !send_cnt || !recv_cnt)))
+        return amgp_fail(AMGP_EINVAL, "amgp_mat_set_halo: bad argument");
+    amgp_ctx *ctx = A->ctx;
+    if (!ctx->comm && npeers) return amgp_fail(AMGP_EINVAL, "context has no communicator");
+    auto *h = new HaloPlan();
+    h->nown = nown;
+    int64_t so = 0, ro = 0;
+    for (int q = 0; q < npeers; q++) {
+        if (peers[q] < 0 || peers[q] >= ctx->nranks || peers[q] == ctx->rank) {
+            halo_free(h);
+            return amgp_fail(AMGP_EINVAL, "bad peer rank");
+        }
+        h->peers.push_back(peers[q]);
+        h->send_cnt.push_back(send_cnt[q]);
+        h->send_off.push_back(so);
+        h->recv_cnt.push_back(recv_cnt[q]);
+        h->recv_off.push_back(ro);
+        so += send_cnt[q];
+        ro += recv_cnt[q];
+    }
+    h->nsend = so;
+    h->nhalo = ro;
+    if (nown + ro != A->ncols) {
+        halo_free(h);
+        return amgp_fail(AMGP_EINVAL, "nown + halo size must equal the local column count");
+    }
+    for (int64_t i = 0; i < so; i++)
+        if (send_idx[i] < 0 || send_idx[i] >= nown) {
+            halo_free(h);
+            return amgp_fail(AMGP_EINVAL, "send index outside the owned range");
+        }
+    // interior slices touch only owned columns; boundary slices touch the halo
+    std::vector<int32_t> in, bd;
+    for (int64_t s = 0; s < A->nslices; s++)
+        (A->slice_maxcol[s] >= nown ? bd : in).push_back((int32_t)s);
+    h->n_interior = (int64_t)in.size();
+    h->n_boundary = (int64_t)bd.size();
+    cudaError_t e = cudaSuccess;
+    auto up = [&](void **dst, const void *src, size_t bytes) {
+        if (e != cudaSuccess) return;
+        e = cudaMalloc(dst, std::max<size_t>(bytes, 8));
+        if (e == cudaSuccess && bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+    };
+    up((void **)&h->send_idx, send_idx, so * sizeof(int64_t));
+    up((void **)&h->interior, in.data(), in.size() * sizeof(int32_t));
+    up((void **)&h->boundary, bd.data(), bd.size() * sizeof(int32_t));
+    if (e == cudaSuccess) e = cudaMalloc(&h->sendbuf, std::max<int64_t>(so, 1) * sizeof(double));
+    if (e == cudaSuccess) e = cudaMalloc(&h->halo, std::max<int64_t>(ro, 1) * sizeof(double));
+    if (e != cudaSuccess) {
+        halo_free(h);
+        return amgp_cuda_fail(e, "halo plan upload", __FILE__, __LINE__);
+    }
+    mat_free_halo(A);
+    A->halo = h;
+    return AMGP_OK;
+}
+
+extern "C" int amgp_mat_halo_info(const amgp_mat *A, int64_t *nown, int64_t *nhalo,
+                                  int64_t *n_interior, int64_t *n_boundary) {
+    if (!A) return amgp_fail(AMGP_EINVAL, "null matrix");
+    const HaloPlan *h = A->halo;
+    if (nown) *nown = h ? h->nown : A->ncols;
+    if (nhalo) *nhalo = h ? h->nhalo : 0;
+    if (n_interior) *n_interior = h ? h->n_interior : A->nslices;
+    if (n_boundary) *n_boundary = h ? h->n_boundary : 0;
+    return AMGP_OK;
+}
+
+__global__ void k_pack(int64_t n, const int64_t *__restrict__ idx, const double *__restrict__ x,
+                       double *__restrict__ out) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x)
+        out[i] = x[idx[i]];
+}
+
+int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
+    const HaloPlan &h = *A->halo;
+    NcclApi *api = nccl();
+    if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator for the halo exchange");
+    if (h.nsend > 0) {
+        const unsigned g = (unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 8);
+        k_pack<<<g, 256, 0, ctx->stream>>>(h.nsend, h.send_idx, x, h.sendbuf);
+        AMGP_CHECK_LAUNCH(ctx);
+    }
+    AMGP_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
+    AMGP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
+    ncclComm_t comm = (ncclComm_t)ctx->comm;
+    NCCL_TRY(api->GroupStart());
+    for (size_t q = 0; q < h.peers.size(); q++) {
+        if (h.send_cnt[q] > 0)
+            NCCL_TRY(api->Send(h.sendbuf + h.send_off[q], (size_t)h.send_cnt[q], ncclDouble, h.peers[q],
+                               comm, ctx->comm_stream));
+        if (h.recv_cnt[q] > 0)
+            NCCL_TRY(api->Recv(h.halo + h.recv_off[q], (size_t)h.recv_cnt[q], ncclDouble, h.peers[q],
+                               comm, ctx->comm_stream));
+    }
+    NCCL_TRY(api->GroupEnd());
+    AMGP_CUDA(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
+    return AMGP_OK;
+}
+
+int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A) {
+    (void)A;
+    AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
+    return AMGP_OK;
+}
+
+// Sum of per-rank partials, deterministic: allgather nv doubles per rank,
+// then every rank folds them in rank order.
+__global__ void k_fold_ranks(const double *__restrict__ g, int nranks, int nv, double *out) {
+    const int q = threadIdx.x;
+    if (q >= nv) return;
+    double s = 0.0;
+    for (int r = 0; r < nranks; r++) s = __dadd_rn(s, g[r * nv + q]);
+    out[q] = s;
+}
+
+int allreduce_sum_ordered(amgp_ctx *ctx, const double *local, int nv, double *out) {
+    NcclApi *api = nccl();
+    if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator");
+    if (nv > 16) return amgp_fail(AMGP_EINVAL, "too many reduction values");
+    NCCL_TRY(api->AllGather(local, ctx->gather_buf, (size_t)nv, ncclDouble, (ncclComm_t)ctx->comm,
+                            ctx->stream));
+    k_fold_ranks<<<1, 32, 0, ctx->stream>>>(ctx->gather_buf, ctx->nranks, nv, out);
+    AMGP_CHECK_LAUNCH(ctx);
+    return AMGP_OK;
+}
+
+// ---------------------------------------------------------------- localisation
+// Map global columns of a generated row block to local ones: [own_lo, own_hi)
+// -> c - own_lo; halo segment q [lo_q, hi_q) -> nown + base_q + (c - lo_q).
+__global__ void k_localize(int64_t stored, int32_t *col, int64_t own_lo, int64_t own_hi, int nseg,
+                           const int64_t *__restrict__ seg) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < stored;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = col[e];
+        if (c < 0) continue;
+        int64_t out = -2;
+        if (c >= own_lo && c < own_hi) {
+            out = c - own_lo;
+        } else {
+            const int64_t nown = own_hi - own_lo;
+            for (int q = 0; q < nseg; q++)
+                if (c >= seg[3 * q] && c < seg[3 * q + 1]) out = nown + seg[3 * q + 2] + (c - seg[3 * q]);
+        }
+        col[e] = (int32_t)out;  // -2 marks a column outside every segment (caught below)
+    }
+}
+
+__global__ void k_slice_maxcol(SellView A, int64_t *out, int *bad) {
+    const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    const int lane = threadIdx.x & 31;
+    if (s >= A.nslices) return;
+    const int64_t base = A.slice_ptr[s];
+    const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
+    int64_t mx = -1;
+    for (int j = 0; j < w; j++) {
+        const int32_t c = A.col[base + (int64_t)j * 32 + lane];
+        if (c == -2) atomicExch(bad, 1);
+        mx = max(mx, (int64_t)c);
+    }
+    for (int o = 16; o > 0; o >>= 1) mx = max(mx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
+    if (lane == 0) out[s] = mx;
+}
+
+int refresh_slice_maxcol(amgp_mat *A) {
+    amgp_ctx *ctx = A->ctx;
+    A->slice_maxcol.assign(A->nslices, -1);
+    if (A->nslices == 0) return AMGP_OK;
+    int64_t *d = nullptr;
+    int *bad = nullptr;
+    AMGP_CUDA(cudaMalloc(&d, A->nslices * sizeof(int64_t)));
+    AMGP_CUDA(cudaMalloc(&bad, sizeof(int)));
+    AMGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    k_slice_maxcol<<<grid_for(A->nslices * 32, 256), 256, 0, ctx->stream>>>(view_of(A), d, bad);
+    AMGP_CHECK_LAUNCH(ctx);
+    int hbad = 0;
+    AMGP_CUDA(cudaMemcpyAsync(A->slice_maxcol.data(), d, A->nslices * sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, ctx->stream));
+    AMGP_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
+    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(d);
+    cudaFree(bad);
+    if (hbad) return amgp_fail(AMGP_EINVAL, "column outside the owned range and every halo segment");
+    return AMGP_OK;
+}
+
+extern "C" int amgp_mat_localize(amgp_mat *A, int64_t own_lo, int64_t own_hi, int nseg,
+                                 const int64_t *seg_lo, const int64_t *seg_hi) {
+    if (!A || own_lo < 0 || own_hi < own_lo || nseg < 0)
+        return amgp_fail(AMGP_EINVAL, "amgp_mat_localize: bad argument");
+    amgp_ctx *ctx = A->ctx;
+    std::vector<int64_t> seg(3 * (size_t)std::max(nseg, 1));
+    int64_t base = 0;
+    for (int q = 0; q < nseg; q++) {
+        seg[3 * q] = seg_lo[q];
+        seg[3 * q + 1] = seg_hi[q];
+        seg[3 * q + 2] = base;
+        base += seg_hi[q] - seg_lo[q];
+    }
+    int64_t *dseg = nullptr;
+    AMGP_CUDA(cudaMalloc(&dseg, seg.size() * sizeof(int64_t)));
+    AMGP_CUDA(cudaMemcpy(dseg, seg.data(), seg.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
+    if (A->stored > 0) {
+        const unsigned g = (unsigned)std::min<int64_t>(grid_for(A->stored, 256), 148 * 16);
+        k_localize<<<g, 256, 0, ctx->stream>>>(A->stored, A->col, own_lo, own_hi, nseg, dseg);
+        AMGP_CHECK_LAUNCH(ctx);
+    }
+    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    cudaFree(dseg);
+    A->ncols = (own_hi - own_lo) + base;
+    A->row_offset = 0;  // rows now index the local block; diagonal at column = row
+    return refresh_slice_maxcol(A);
+}

@@ -102,7 +102,12 @@ extern "C" int amgp_mat_from_csr(amgp_ctx *ctx, int64_t nrows, int64_t ncols,
     amgp_mat *A = nullptr;
     AMGP_TRY(mat_alloc(ctx, nrows, ncols, row_ptr[nrows], ns, stored, &A));
     int32_t wmax = 0;
-    for (int64_t s = 0; s < ns; s++) wmax = std::max<int32_t>(wmax, (int32_t)((sp[s + 1] - sp[s]) / AMGP_SLICE));
+    A->slice_maxcol.assign(ns, -1);
+    for (int64_t s = 0; s < ns; s++) {
+        wmax = std::max<int32_t>(wmax, (int32_t)((sp[s + 1] - sp[s]) / AMGP_SLICE));
+        for (int64_t e = sp[s]; e < sp[s + 1]; e++)
+            A->slice_maxcol[s] = std::max<int64_t>(A->slice_maxcol[s], col[e]);
+    }
     A->max_width = wmax;
     cudaError_t e = cudaMemcpy(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && stored > 0)
@@ -123,6 +128,7 @@ extern "C" int amgp_mat_destroy(amgp_mat *A) {
         cudaSetDevice(A->ctx->device);
         cudaStreamSynchronize(A->ctx->stream);
     }
+    mat_free_halo(A);
     cudaFree(A->slice_ptr);
     cudaFree(A->col);
     cudaFree(A->val);
@@ -304,6 +310,11 @@ extern "C" int amgp_mat_poisson3d(amgp_ctx *ctx, int64_t m, int stencil, int64_t
         i += run;
     }
     A->nnz = nnz;
+    int st = refresh_slice_maxcol(A);
+    if (st != AMGP_OK) {
+        amgp_mat_destroy(A);
+        return st;
+    }
     *out = A;
     return AMGP_OK;
 }
@@ -360,9 +371,9 @@ __global__ void k_l1_diag(SellView A, int64_t row_offset, double *__restrict__ m
 extern "C" int amgp_mat_l1_diag(amgp_mat *A, double *m_dev) {
     if (!A || !m_dev) return amgp_fail(AMGP_EINVAL, "amgp_mat_l1_diag: bad argument");
     amgp_ctx *ctx = A->ctx;
-    if (A->row_offset == 0 && A->nrows != A->ncols)
-        return amgp_fail(AMGP_EINVAL, "matrix must be square");
-    if (A->row_offset + A->nrows > A->ncols) return amgp_fail(AMGP_EINVAL, "bad row block");
+    // square matrix, or a row block (generated: global columns from
+    // row_offset; localized: own columns first, halo after)
+    if (A->row_offset + A->nrows > A->ncols) return amgp_fail(AMGP_EINVAL, "matrix must be square");
     int *bad = nullptr;
     AMGP_CUDA(cudaMalloc(&bad, sizeof(int)));
     AMGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));

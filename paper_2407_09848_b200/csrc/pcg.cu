@@ -5,36 +5,75 @@
 // Dots are deterministic: a fixed grid, per-thread sequential partials,
 // xor-butterfly warp sums, a fixed block tree, and the last block to finish
 // (atomic ticket) folds the per-block partials in block order -- the same
-// bits on every run.  Their order differs from OpenBLAS ddot, hence the
-// reference's +-1 iteration tolerance.
+// bits on every run.  Across GPUs the per-rank totals are all-gathered and
+// folded in rank order (dist.cu), so every rank holds identical scalars.
+// The dot order differs from OpenBLAS ddot, hence the reference's +-1
+// iteration tolerance.
 //
 // One iteration (fusions in brackets):
 //   [Ad = A d ; d.Ad (; r.d)] -> dAd, alpha, breakdown          k_pcg_spmv_dot
+//       (distributed: halo-exchanged SpMV, then k_pcg_dot2)
 //   [x += alpha d ; r -= alpha Ad ; r.r] -> relres              k_pcg_update
 //   z = V(r)                                                    V-cycle graph
 //   [r.z | z.Ad] -> beta                                        k_pcg_dot
 //   d = z +- beta d                                             k_pcg_dir
-// The host checks relres while the GPU already runs the (harmless when the
-// iteration turns out to be the last) V-cycle and direction update.
 #include <math.h>
-#include <time.h>
 
 #include <algorithm>
 #include <chrono>
 
-#include "amgp_common.cuh"
+#include "rows.cuh"
 
 int vcycle_enqueue(amgp_hier *h, const double *r, double *z);
 int64_t hier_rows(const amgp_hier *h);
 std::mutex &hier_mutex(amgp_hier *h);
+int allreduce_sum_ordered(amgp_ctx *ctx, const double *local, int nv, double *out);
 
 enum {
     S_BNORM = 0, S_RZ, S_DAD, S_ALPHA, S_BETA, S_RELRES, S_BRK, S_RR, S_BB, S_AUX,
-    S_COUNT
+    S_COUNT,
+    S_LOC = 16,  // per-rank reduction totals (distributed)
+    S_GLB = 32   // rank-folded totals
 };
+
+// what the folded totals of a reduction become (krylov.py line numbers)
+enum { OP_BNORM, OP_RELRES, OP_RZ, OP_DAD, OP_DAD_FCG, OP_BETA, OP_BETA_FCG };
 
 #define RB 256          // reduction block
 #define RGRID_MAX 1184  // 148 SMs x 8
+
+__device__ __forceinline__ void apply_op(int op, const double *t, double *sc) {
+    switch (op) {
+        case OP_BNORM:  // :67
+            sc[S_BNORM] = sqrt(t[0]);
+            sc[S_BRK] = 0.0;
+            break;
+        case OP_RELRES:  // :75, :103
+            sc[S_RELRES] = __ddiv_rn(sqrt(t[0]), sc[S_BNORM]);
+            break;
+        case OP_RZ:  // :92
+            sc[S_RZ] = t[0];
+            sc[S_BRK] = 0.0;
+            break;
+        case OP_DAD:
+        case OP_DAD_FCG: {  // :96-100
+            const double dAd = t[0];
+            sc[S_DAD] = dAd;
+            if (dAd <= 0.0) sc[S_BRK] = 1.0;
+            sc[S_ALPHA] = op == OP_DAD_FCG ? __ddiv_rn(t[1], dAd) : __ddiv_rn(sc[S_RZ], dAd);
+            break;
+        }
+        case OP_BETA:  // :111-113
+            sc[S_BETA] = __ddiv_rn(t[0], sc[S_RZ]);
+            sc[S_RZ] = t[0];
+            break;
+        case OP_BETA_FCG:  // :118
+            sc[S_BETA] = __ddiv_rn(t[0], sc[S_DAD]);
+            break;
+    }
+}
+
+__global__ void k_apply_op(int op, double *sc) { apply_op(op, sc + S_GLB, sc); }
 
 __device__ __forceinline__ double block_sum(double v) {
     __shared__ double ws[RB / 32];
@@ -50,11 +89,11 @@ __device__ __forceinline__ double block_sum(double v) {
     return v;  // valid in warp 0
 }
 
-// Publish this block's partial(s); returns true in the last block, whose
-// thread 0 then holds the folded totals in tot[0..NV-1].
+// Publish this block's partial(s); the last block folds them in block order
+// and either applies `op` (single GPU) or stores the rank totals at S_LOC.
 template <int NV>
-__device__ bool reduce_partials(const double (&acc)[NV], double *partial, unsigned *ticket,
-                                double (&tot)[NV]) {
+__device__ void reduce_finish(const double (&acc)[NV], double *partial, unsigned *ticket, int op,
+                              bool dist, double *sc) {
     __shared__ bool last;
     double bs[NV];
 #pragma unroll
@@ -66,8 +105,9 @@ __device__ bool reduce_partials(const double (&acc)[NV], double *partial, unsign
         last = atomicAdd(ticket, 1u) == gridDim.x - 1;
     }
     __syncthreads();
-    if (!last) return false;
+    if (!last) return;
     __threadfence();
+    double tot[NV];
 #pragma unroll
     for (int q = 0; q < NV; q++) {
         double t = 0.0;
@@ -75,27 +115,35 @@ __device__ bool reduce_partials(const double (&acc)[NV], double *partial, unsign
             t = __dadd_rn(t, __ldcg(partial + q * RGRID_MAX + i));
         tot[q] = block_sum(t);
     }
-    if (threadIdx.x == 0) *ticket = 0;
-    return threadIdx.x == 0;
-}
-
-// MODE 0: S_BB = b.b -> bnorm ; MODE 1: r.r -> relres ; MODE 2: r.z -> rz (init)
-template <int MODE>
-__global__ void __launch_bounds__(RB)
-k_pcg_dot_init(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
-               double *partial, unsigned *ticket, double *sc) {
-    double acc[1] = {0.0};
-    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
-        acc[0] = __dadd_rn(acc[0], __dmul_rn(a[i], b[i]));
-    double tot[1];
-    if (reduce_partials<1>(acc, partial, ticket, tot)) {
-        if (MODE == 0) sc[S_BNORM] = sqrt(tot[0]);
-        else if (MODE == 1) sc[S_RELRES] = __ddiv_rn(sqrt(tot[0]), sc[S_BNORM]);
-        else sc[S_RZ] = tot[0];
-        sc[S_BRK] = 0.0;
+    if (threadIdx.x == 0) {
+        *ticket = 0;
+        if (dist) {
+#pragma unroll
+            for (int q = 0; q < NV; q++) sc[S_LOC + q] = tot[q];
+        } else {
+            apply_op(op, tot, sc);
+        }
     }
 }
 
+// sum_i a_i b_i (and, with NV = 2, sum_i c_i d_i)
+template <int NV>
+__global__ void __launch_bounds__(RB)
+k_pcg_dot2(int64_t n, const double *__restrict__ a, const double *__restrict__ b,
+           const double *__restrict__ c, const double *__restrict__ d, double *partial,
+           unsigned *ticket, double *sc, int op, int dist, int skip_on_breakdown) {
+    if (skip_on_breakdown && sc[S_BRK] != 0.0) return;
+    double acc[NV];
+#pragma unroll
+    for (int q = 0; q < NV; q++) acc[q] = 0.0;
+    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(a[i], b[i]));
+        if (NV > 1) acc[NV - 1] = __dadd_rn(acc[NV - 1], __dmul_rn(c[i], d[i]));
+    }
+    reduce_finish<NV>(acc, partial, ticket, op, dist, sc);
+}
+
+// single-GPU fused Ad = A d ; d.Ad (; r.d)
 template <bool FCG>
 __global__ void __launch_bounds__(RB)
 k_pcg_spmv_dot(SellView A, const double *__restrict__ d, double *__restrict__ Ad,
@@ -113,51 +161,23 @@ k_pcg_spmv_dot(SellView A, const double *__restrict__ d, double *__restrict__ Ad
             if (FCG) acc[1] = __dadd_rn(acc[1], __dmul_rn(r[row], di));
         }
     }
-    double tot[2];
-    if (reduce_partials<2>(acc, partial, ticket, tot)) {
-        const double dAd = tot[0];
-        sc[S_DAD] = dAd;
-        if (dAd <= 0.0) sc[S_BRK] = 1.0;                      // krylov.py:97-99
-        sc[S_ALPHA] = FCG ? __ddiv_rn(tot[1], dAd) : __ddiv_rn(sc[S_RZ], dAd);  // :100
-    }
+    reduce_finish<2>(acc, partial, ticket, FCG ? OP_DAD_FCG : OP_DAD, false, sc);
 }
 
 __global__ void __launch_bounds__(RB)
 k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
              const double *__restrict__ d, const double *__restrict__ Ad, double *partial,
-             unsigned *ticket, double *sc) {
+             unsigned *ticket, double *sc, int dist) {
     if (sc[S_BRK] != 0.0) return;  // breakdown: x, r stay as the reference returns them
     const double alpha = sc[S_ALPHA];
     double acc[1] = {0.0};
     for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
-        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, d[i]));   // krylov.py:101
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, d[i]));             // krylov.py:101
         const double ri = __dsub_rn(r[i], __dmul_rn(alpha, Ad[i]));  // :102
         r[i] = ri;
         acc[0] = __dadd_rn(acc[0], __dmul_rn(ri, ri));
     }
-    double tot[1];
-    if (reduce_partials<1>(acc, partial, ticket, tot))
-        sc[S_RELRES] = __ddiv_rn(sqrt(tot[0]), sc[S_BNORM]);  // :103
-}
-
-template <bool FCG>
-__global__ void __launch_bounds__(RB)
-k_pcg_dot(int64_t n, const double *__restrict__ r, const double *__restrict__ z,
-          const double *__restrict__ Ad, double *partial, unsigned *ticket, double *sc) {
-    if (sc[S_BRK] != 0.0) return;
-    double acc[1] = {0.0};
-    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB)
-        acc[0] = FCG ? __dadd_rn(acc[0], __dmul_rn(z[i], Ad[i]))
-                     : __dadd_rn(acc[0], __dmul_rn(r[i], z[i]));
-    double tot[1];
-    if (reduce_partials<1>(acc, partial, ticket, tot)) {
-        if (FCG) {
-            sc[S_BETA] = __ddiv_rn(tot[0], sc[S_DAD]);  // krylov.py:118
-        } else {
-            sc[S_BETA] = __ddiv_rn(tot[0], sc[S_RZ]);   // :111-113
-            sc[S_RZ] = tot[0];
-        }
-    }
+    reduce_finish<1>(acc, partial, ticket, OP_RELRES, dist, sc);
 }
 
 template <bool FCG>
@@ -221,7 +241,8 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     if (variant != AMGP_PCG && variant != AMGP_FCG)
         return amgp_fail(AMGP_EINVAL, "unknown Krylov variant");
     if (!(tol > 0.0) || itmax < 1) return amgp_fail(AMGP_EINVAL, "tol must be positive and itmax >= 1");
-    if (A->nrows != A->ncols) return amgp_fail(AMGP_EINVAL, "matrix must be square");
+    const int64_t nown = A->halo ? A->halo->nown : A->ncols;
+    if (A->nrows != nown) return amgp_fail(AMGP_EINVAL, "matrix must be square");
     if (h && hier_rows(h) != A->nrows) return amgp_fail(AMGP_EINVAL, "dimension mismatch");
     const int64_t n = A->nrows;
     if (n > 0 && (!b || !x)) return amgp_fail(AMGP_EINVAL, "null vector");
@@ -232,6 +253,7 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
         return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     };
     const bool fcg = variant == AMGP_FCG;
+    const bool dist = ctx->comm != nullptr && ctx->nranks > 1;
     cudaStream_t st = ctx->stream;
     double *sc = ctx->scalars, *hs = ctx->host_scalars;
 
@@ -240,6 +262,23 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     AMGP_TRY(pcg_workspace(ctx, n, &w));
     const unsigned g = rgrid(n);
     const unsigned gs = (unsigned)std::max<int64_t>(1, std::min<int64_t>(grid_for(A->nslices, RB / 32), RGRID_MAX));
+
+    // one reduction: launch the kernel; across ranks, fold the totals and
+    // apply the op on every rank
+    auto dot = [&](int nv, const double *a, const double *bb, const double *c, const double *d,
+                   int op, int skip_brk) -> int {
+        if (nv == 1)
+            k_pcg_dot2<1><<<g, RB, 0, st>>>(n, a, bb, c, d, w.partial, w.ticket, sc, op, dist, skip_brk);
+        else
+            k_pcg_dot2<2><<<g, RB, 0, st>>>(n, a, bb, c, d, w.partial, w.ticket, sc, op, dist, skip_brk);
+        AMGP_CHECK_LAUNCH(ctx);
+        if (dist) {
+            AMGP_TRY(allreduce_sum_ordered(ctx, sc + S_LOC, nv, sc + S_GLB));
+            k_apply_op<<<1, 1, 0, st>>>(op, sc);
+            AMGP_CHECK_LAUNCH(ctx);
+        }
+        return AMGP_OK;
+    };
 
     *rep = amgp_solve_report{};
     int nh = 0;
@@ -250,8 +289,7 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     };
 
     if (!x0_given) AMGP_CUDA(cudaMemsetAsync(x, 0, nb, st));
-    k_pcg_dot_init<0><<<g, RB, 0, st>>>(n, b, b, w.partial, w.ticket, sc);  // bnorm
-    AMGP_CHECK_LAUNCH(ctx);
+    AMGP_TRY(dot(1, b, b, nullptr, nullptr, OP_BNORM, 0));  // bnorm (:67)
     AMGP_TRY(fetch());
     if (hs[S_BNORM] == 0.0) {  // krylov.py:68-69
         k_scale_zero<<<g, RB, 0, st>>>(n, x);
@@ -263,8 +301,7 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     }
     AMGP_TRY(residual_enqueue(ctx, A, b, x, w.r));  // r = b - A x (:71)
     int spmv = 1, pc = 0;
-    k_pcg_dot_init<1><<<g, RB, 0, st>>>(n, w.r, w.r, w.partial, w.ticket, sc);
-    AMGP_CHECK_LAUNCH(ctx);
+    AMGP_TRY(dot(1, w.r, w.r, nullptr, nullptr, OP_RELRES, 0));
     AMGP_TRY(fetch());
     double relres = hs[S_RELRES];
     if (history) history[nh] = relres;
@@ -292,15 +329,13 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     AMGP_TRY(precond());
     pc++;
     AMGP_CUDA(cudaMemcpyAsync(w.d, w.z, nb, cudaMemcpyDeviceToDevice, st));
-    k_pcg_dot_init<2><<<g, RB, 0, st>>>(n, w.r, w.z, w.partial, w.ticket, sc);  // rz
-    AMGP_CHECK_LAUNCH(ctx);
+    AMGP_TRY(dot(1, w.r, w.z, nullptr, nullptr, OP_RZ, 0));  // rz (:92)
 
     // next preconditioner application + direction update (krylov.py:108-119)
     auto next_direction = [&]() -> int {
         AMGP_TRY(precond());
-        if (fcg) k_pcg_dot<true><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
-        else k_pcg_dot<false><<<g, RB, 0, st>>>(n, w.r, w.z, w.Ad, w.partial, w.ticket, sc);
-        AMGP_CHECK_LAUNCH(ctx);
+        if (fcg) AMGP_TRY(dot(1, w.z, w.Ad, nullptr, nullptr, OP_BETA_FCG, 1));
+        else AMGP_TRY(dot(1, w.r, w.z, nullptr, nullptr, OP_BETA, 1));
         if (fcg) k_pcg_dir<true><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
         else k_pcg_dir<false><<<g, RB, 0, st>>>(n, w.z, w.d, sc);
         AMGP_CHECK_LAUNCH(ctx);
@@ -313,12 +348,23 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     AMGP_CUDA(cudaEventCreateWithFlags(&ev.e, cudaEventDisableTiming));
     double rel_prev = relres, rel_prev2 = -1.0;
     for (int it = 1; it <= itmax; it++) {
-        if (fcg) k_pcg_spmv_dot<true><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
-        else k_pcg_spmv_dot<false><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
-        AMGP_CHECK_LAUNCH(ctx);
+        if (!dist && !A->halo) {
+            if (fcg) k_pcg_spmv_dot<true><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
+            else k_pcg_spmv_dot<false><<<gs, RB, 0, st>>>(view_of(A), w.d, w.Ad, w.r, w.partial, w.ticket, sc);
+            AMGP_CHECK_LAUNCH(ctx);
+        } else {
+            AMGP_TRY(spmv_enqueue(ctx, A, w.d, w.Ad));
+            if (fcg) AMGP_TRY(dot(2, w.d, w.Ad, w.r, w.d, OP_DAD_FCG, 0));
+            else AMGP_TRY(dot(1, w.d, w.Ad, nullptr, nullptr, OP_DAD, 0));
+        }
         spmv++;
-        k_pcg_update<<<g, RB, 0, st>>>(n, x, w.r, w.d, w.Ad, w.partial, w.ticket, sc);
+        k_pcg_update<<<g, RB, 0, st>>>(n, x, w.r, w.d, w.Ad, w.partial, w.ticket, sc, dist);
         AMGP_CHECK_LAUNCH(ctx);
+        if (dist) {  // after a breakdown k_pcg_update returned early: keep relres
+            AMGP_TRY(allreduce_sum_ordered(ctx, sc + S_LOC, 1, sc + S_GLB));
+            k_apply_op<<<1, 1, 0, st>>>(OP_RELRES, sc);
+            AMGP_CHECK_LAUNCH(ctx);
+        }
         AMGP_CUDA(cudaMemcpyAsync(hs, sc, S_COUNT * sizeof(double), cudaMemcpyDeviceToHost, st));
         AMGP_CUDA(cudaEventRecord(ev.e, st));
         // While the host waits for relres, keep the GPU busy with the next

@@ -30,9 +30,10 @@
 template <class Epi>
 __global__ void __launch_bounds__(ROWS_BLOCK)
 k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
-    const int64_t s = (int64_t)blockIdx.x * ROWS_SLICES + (threadIdx.x >> 5);
+    const int64_t idx = (int64_t)blockIdx.x * ROWS_SLICES + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (s >= A.nslices) return;
+    if (idx >= A.nlist) return;
+    const int64_t s = A.slist ? (int64_t)A.slist[idx] : idx;
     double y = 0.0;
     if (Epi::kSpmv) y = sell_row_dot<ROWS_U>(A, s, lane, xg);
     const int64_t row = s * 32 + lane;
@@ -43,7 +44,7 @@ template <class Epi>
 __global__ void __launch_bounds__(SPLIT_WARPS * 32)
 k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     __shared__ double prod[SPLIT_CHUNK * 32];
-    const int64_t s = blockIdx.x;
+    const int64_t s = A.slist ? (int64_t)A.slist[blockIdx.x] : (int64_t)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
@@ -65,8 +66,13 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
 #pragma unroll
             for (int u = 0; u < 4; u++) {
                 const int jj = j + u * SPLIT_WARPS;
-                if (jj < jn)
-                    prod[jj * 32 + lane] = cc[u] >= 0 ? __dmul_rn(vv[u], ld_gather_f64(xg + cc[u], pl)) : 0.0;
+                if (jj < jn) {
+                    double p = 0.0;
+                    if (cc[u] >= 0)
+                        p = __dmul_rn(vv[u], cc[u] < A.nown ? ld_gather_f64(xg + cc[u], pl)
+                                                            : ld_gather_f64(A.xh + (cc[u] - A.nown), pl));
+                    prod[jj * 32 + lane] = p;
+                }
             }
         }
         __syncthreads();
@@ -87,12 +93,34 @@ inline bool use_split(const amgp_mat *A) {
 }
 
 template <class Epi>
-int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &epi) {
-    if (A->nslices == 0) return AMGP_OK;
+int launch_view(amgp_ctx *ctx, const amgp_mat *A, const SellView &v, const double *xg,
+                const Epi &epi) {
+    if (v.nlist == 0) return AMGP_OK;
     if (Epi::kSpmv && use_split(A))
-        k_split_rows<Epi><<<(unsigned)A->nslices, SPLIT_WARPS * 32, 0, ctx->stream>>>(view_of(A), xg, epi);
+        k_split_rows<Epi><<<(unsigned)v.nlist, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
     else
-        k_thread_rows<Epi><<<grid_for(A->nslices, ROWS_SLICES), ROWS_BLOCK, 0, ctx->stream>>>(view_of(A), xg, epi);
+        k_thread_rows<Epi><<<grid_for(v.nlist, ROWS_SLICES), ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
+}
+
+// y-rows of A with epilogue epi, gathering operand xg.  For a distributed
+// matrix the halo of xg travels over NCCL on the comm stream while the
+// interior slices (no halo column) compute; boundary slices run after.
+template <class Epi>
+int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &epi) {
+    if (A->nslices == 0) return AMGP_OK;
+    if (!Epi::kSpmv || !A->halo) return launch_view(ctx, A, view_of(A), xg, epi);
+    const HaloPlan &h = *A->halo;
+    AMGP_TRY(halo_exchange_begin(ctx, A, xg));
+    SellView v = view_of(A);
+    v.nown = h.nown;
+    v.xh = h.halo;
+    v.slist = h.interior;
+    v.nlist = h.n_interior;
+    AMGP_TRY(launch_view(ctx, A, v, xg, epi));
+    AMGP_TRY(halo_exchange_end(ctx, A));
+    v.slist = h.boundary;
+    v.nlist = h.n_boundary;
+    return launch_view(ctx, A, v, xg, epi);
 }

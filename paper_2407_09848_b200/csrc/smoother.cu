@@ -249,7 +249,8 @@ extern "C" int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
                                    const amgp_smoother_cfg *cfg, const double *b,
                                    const double *x0, double *x) {
     if (!ctx || !A || !cfg) return amgp_fail(AMGP_EINVAL, "amgp_smoother_apply: bad argument");
-    if (A->nrows != A->ncols) return amgp_fail(AMGP_EINVAL, "dimension mismatch");
+    if (A->nrows != (A->halo ? A->halo->nown : A->ncols))
+        return amgp_fail(AMGP_EINVAL, "dimension mismatch");
     if (A->nrows > 0 && (!m || !b || !x)) return amgp_fail(AMGP_EINVAL, "null vector");
     SmootherPlan p;
     AMGP_TRY(make_smoother_plan(cfg, &p));

@@ -137,7 +137,7 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
     }
     if (h->coarse_solver == AMGP_COARSE_SMOOTHER)
         return smoother_enqueue(ctx, A, h->m[l], h->plan[l], r, nullptr, z, h->work[l]);
-    if (coarse_smem(A) <= COARSE_SMEM_BYTES) {
+    if (!A->halo && coarse_smem(A) <= COARSE_SMEM_BYTES) {
         k_coarse_l1<<<1, 1024, coarse_smem(A), ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
@@ -211,13 +211,15 @@ extern "C" int amgp_hier_create(amgp_ctx *ctx, int nlevels, amgp_mat *const *A,
         coarse_solver != AMGP_COARSE_SMOOTHER)
         return amgp_fail(AMGP_EINVAL, "unknown coarse solver");
     if (coarse_sweeps < 1) return amgp_fail(AMGP_EINVAL, "coarse_sweeps must be >= 1");
+    // operand length of a (possibly distributed) matrix: its own columns
+    auto own = [](const amgp_mat *M) { return M->halo ? M->halo->nown : M->ncols; };
     for (int l = 0; l < nlevels; l++) {
-        if (!A[l] || A[l]->nrows != A[l]->ncols || (A[l]->nrows > 0 && !m[l]))
+        if (!A[l] || A[l]->nrows != own(A[l]) || (A[l]->nrows > 0 && !m[l]))
             return amgp_fail(AMGP_EINVAL, "level matrix must be square with a diagonal");
         if (l < nlevels - 1) {
             if (!P || !R || !P[l] || !R[l]) return amgp_fail(AMGP_EINVAL, "missing prolongator");
-            if (P[l]->nrows != A[l]->nrows || P[l]->ncols != A[l + 1]->nrows ||
-                R[l]->nrows != A[l + 1]->nrows || R[l]->ncols != A[l]->nrows)
+            if (P[l]->nrows != A[l]->nrows || own(P[l]) != A[l + 1]->nrows ||
+                R[l]->nrows != A[l + 1]->nrows || own(R[l]) != A[l]->nrows)
                 return amgp_fail(AMGP_EINVAL, "dimension mismatch in prolongator");
         }
     }

@@ -91,7 +91,12 @@ extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const cha
     ctx->comm = comm;
     ctx->nranks = nranks;
     ctx->rank = rank;
-    AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    // Highest priority: the NCCL kernels of a halo exchange become ready at
+    // the same moment as the interior-rows kernel and must get their SMs
+    // first, or the exchange would wait for the interior kernel to drain.
+    int least = 0, greatest = 0;
+    AMGP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    AMGP_CUDA(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, greatest));
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_exchanged, cudaEventDisableTiming));
     AMGP_CUDA(cudaMalloc(&ctx->gather_buf, (size_t)nranks * 16 * sizeof(double)));

@@ -24,7 +24,7 @@ sys.path.insert(0, os.path.join(REPO, "oracle"))
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--m", type=int, default=32)
+    ap.add_argument("--grid", type=int, default=32)
     ap.add_argument("--replicate-below", type=int, default=2000)
     ap.add_argument("--graph", action="store_true")
     args = ap.parse_args()
@@ -42,7 +42,7 @@ def main():
     comm = D.Communicator(local)
     me, world = comm.rank, comm.size
     out = {"rank": me, "world": world, "ok": True, "checks": {}}
-    m = args.m
+    m = args.grid
     fams = ("l1_jacobi", "cheb4", "opt_cheb4", "opt_cheb1")
 
     # 1. fine-level row block

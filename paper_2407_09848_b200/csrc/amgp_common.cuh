@@ -82,6 +82,11 @@ struct HaloPlan {
     double *halo = nullptr;                       // device [nhalo]
     int32_t *interior = nullptr, *boundary = nullptr;  // device slice lists
     int64_t n_interior = 0, n_boundary = 0;
+    // the same sets as runs of consecutive slices (first, count); when a set
+    // has few runs (row-block partitions of banded levels: interior = one
+    // run, boundary = the two block ends) kernels index slices directly
+    // instead of through the list
+    std::vector<std::pair<int64_t, int64_t>> interior_runs, boundary_runs;
 };
 
 struct amgp_mat {
@@ -108,15 +113,16 @@ struct SellView {
     const double *__restrict__ val;
     int64_t nrows;
     int64_t nslices;
-    const int32_t *__restrict__ slist;  // slices to process (nullptr: 0..nlist-1)
+    const int32_t *__restrict__ slist;  // slices to process (nullptr: s0 .. s0+nlist-1)
     int64_t nlist;
     int64_t nown;                       // gathers of columns >= nown read xh
     const double *__restrict__ xh;
+    int64_t s0;                         // first slice of a contiguous run
 };
 
 inline SellView view_of(const amgp_mat *A) {
     return SellView{A->slice_ptr, A->col, A->val, A->nrows, A->nslices,
-                    nullptr,      A->nslices, INT64_MAX, nullptr};
+                    nullptr,      A->nslices, INT64_MAX, nullptr, 0};
 }
 
 // Exchange the halo of operand x (own part) for a distributed matrix; after

@@ -166,6 +166,16 @@ extern "C" int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const in
         (A->slice_maxcol[s] >= nown ? bd : in).push_back((int32_t)s);
     h->n_interior = (int64_t)in.size();
     h->n_boundary = (int64_t)bd.size();
+    auto runs = [](const std::vector<int32_t> &s) {
+        std::vector<std::pair<int64_t, int64_t>> r;
+        for (int32_t x : s) {
+            if (!r.empty() && r.back().first + r.back().second == x) r.back().second++;
+            else r.emplace_back(x, 1);
+        }
+        return r;
+    };
+    h->interior_runs = runs(in);
+    h->boundary_runs = runs(bd);
     cudaError_t e = cudaSuccess;
     auto up = [&](void **dst, const void *src, size_t bytes) {
         if (e != cudaSuccess) return;

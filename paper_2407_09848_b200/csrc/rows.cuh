@@ -33,7 +33,7 @@ k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     const int64_t idx = (int64_t)blockIdx.x * ROWS_SLICES + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (idx >= A.nlist) return;
-    const int64_t s = A.slist ? (int64_t)A.slist[idx] : idx;
+    const int64_t s = A.slist ? (int64_t)A.slist[idx] : A.s0 + idx;
     double y = 0.0;
     if (Epi::kSpmv) y = sell_row_dot<ROWS_U>(A, s, lane, xg);
     const int64_t row = s * 32 + lane;
@@ -44,7 +44,7 @@ template <class Epi>
 __global__ void __launch_bounds__(SPLIT_WARPS * 32)
 k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     __shared__ double prod[SPLIT_CHUNK * 32];
-    const int64_t s = A.slist ? (int64_t)A.slist[blockIdx.x] : (int64_t)blockIdx.x;
+    const int64_t s = A.slist ? (int64_t)A.slist[blockIdx.x] : A.s0 + (int64_t)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
@@ -116,11 +116,24 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     SellView v = view_of(A);
     v.nown = h.nown;
     v.xh = h.halo;
-    v.slist = h.interior;
-    v.nlist = h.n_interior;
-    AMGP_TRY(launch_view(ctx, A, v, xg, epi));
+    // one launch per run when the set is a few contiguous runs, else the list
+    auto launch_set = [&](const std::vector<std::pair<int64_t, int64_t>> &runs,
+                          const int32_t *list, int64_t n) -> int {
+        if (runs.size() <= 2) {
+            for (const auto &r : runs) {
+                v.slist = nullptr;
+                v.s0 = r.first;
+                v.nlist = r.second;
+                AMGP_TRY(launch_view(ctx, A, v, xg, epi));
+            }
+            return AMGP_OK;
+        }
+        v.slist = list;
+        v.s0 = 0;
+        v.nlist = n;
+        return launch_view(ctx, A, v, xg, epi);
+    };
+    AMGP_TRY(launch_set(h.interior_runs, h.interior, h.n_interior));
     AMGP_TRY(halo_exchange_end(ctx, A));
-    v.slist = h.boundary;
-    v.nlist = h.n_boundary;
-    return launch_view(ctx, A, v, xg, epi);
+    return launch_set(h.boundary_runs, h.boundary, h.n_boundary);
 }

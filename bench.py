@@ -58,7 +58,7 @@ def peaks():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
-    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+    FIELDS = ("timestamp,clocks.sm,clocks.max.sm,clocks.mem,power.draw,clocks_event_reasons.active,"
               "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
               "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
 
@@ -99,7 +99,7 @@ class ClockSampler:
         with open(self.f.name) as fh:
             for line in fh:
                 p = [x.strip() for x in line.split(",")]
-                if len(p) >= 9:
+                if len(p) >= 10:
                     try:
                         p[0] = datetime.datetime.strptime(p[0], "%Y/%m/%d %H:%M:%S.%f").timestamp()
                     except ValueError:
@@ -124,10 +124,12 @@ class ClockSampler:
 
         sm = [num(r[1]) for r in rows if num(r[1]) is not None]
         mx = [num(r[2]) for r in rows if num(r[2]) is not None]
+        mem = [num(r[3]) for r in rows if num(r[3]) is not None]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i] == "Active"})
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[6 + i] == "Active"})
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "sm_max_mhz": max(mx) if mx else None,
+                "mem_mhz": statistics.median(mem) if mem else None, "reasons": reasons,
                 "samples": len(rows), "window": window}
 
 
@@ -297,6 +299,55 @@ def solve_bench(m, kind="smoothed_aggregation", cpu=True):
     return out
 
 
+def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4):
+    """Weak-scaled PCG + AMG solve over all ranks (BASELINE configs[3] shape):
+    global cube round(m_base N^(1/3)), hierarchy built once on rank 0 (native
+    setup) and shared, every level row-partitioned (coarse levels
+    replicated).  Returns (on every rank) iterations and max-over-ranks time."""
+    import torch
+    import torch.distributed as dist
+
+    import paper_2407_09848_b200 as P
+    from paper_2407_09848_b200 import dist as Dist
+
+    m = int(round(m_base * ws ** (1.0 / 3.0)))
+    cfg = P.PolySmootherConfig(family=family, degree=k)
+    t0 = time.perf_counter()
+
+    def build():
+        A, _ = P.poisson3d(m)
+        return P.build_hierarchy(A, smoother=cfg)
+
+    d, path = Dist.share_hierarchy(build, comm.rank, dist.barrier)
+    setup_s = time.perf_counter() - t0
+    dh = Dist.DistHierarchy(d, comm, cfg)
+    lo, hi = dh.row_range
+    bd = torch.ones(hi - lo, dtype=torch.float64, device="cuda")
+    kc = P.KrylovConfig(tol=1e-6, itmax=1000)
+    dh.solve(bd, cfg=kc)  # warm-up
+    torch.cuda.synchronize()
+    dist.barrier()
+    c = dh.ctx
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(c.stream)
+    x, rep = dh.solve(bd, cfg=kc)
+    e1.record(c.stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) / 1e3, rep.elapsed_s], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    dist.barrier()
+    if comm.rank == 0:
+        try:
+            os.unlink(path)
+        except OSError:
+            pass
+    return {"m": m, "n": int(m ** 3), "rows_per_gpu": hi - lo, "family": family, "degree": k,
+            "levels": [int(d[f"A{l}_shape"][0]) for l in range(int(d["nlev"][0]))],
+            "distributed_levels": sum(p is not None for p in dh.parts),
+            "setup_s": setup_s, "iterations": rep.iterations, "final_relres": rep.final_relres,
+            "solve_s": float(t[0].item()), "wall_s": float(t[1].item()), "tol": 1e-6}
+
+
 def run_b200(args):
     import torch
     import torch.distributed as dist
@@ -410,6 +461,10 @@ def run_b200(args):
     e2e = {"value": job_step_bytes / e2e_s / 1e9, "unit": "GB/s",
            "h2d_bytes_per_step": len(cfgs) * 2 * n * 8, "d2h_bytes_per_step": len(cfgs) * n * 8}
 
+    dsolve = None
+    if ws > 1 and args.solve_m > 0:
+        dsolve = dist_solve_bench(comm, args.solve_m, ws)
+
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": ws,
@@ -440,6 +495,8 @@ def run_b200(args):
             line["cpu_baseline"] = cpu_baseline(args.cpu_m)
         if ws == 1 and args.solve_m > 0:
             line["solve"] = solve_bench(args.solve_m, cpu=not args.no_cpu_baseline)
+        if dsolve is not None:
+            line["solve"] = dsolve
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()

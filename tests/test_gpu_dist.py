@@ -1,0 +1,52 @@
+"""Multi-GPU parity (needs >= 2 GPUs): runs tools/dist_check.py under torchrun.
+
+Bitwise smoother apply on generated row blocks and bitwise V-cycles of a
+row-partitioned native hierarchy against the C oracle; distributed PCG/FCG
+iteration counts equal to the oracle's (+-1 bar).
+"""
+
+import json
+import os
+import socket
+import subprocess
+import sys
+
+import pytest
+
+from conftest import REPO
+
+pytestmark = pytest.mark.gpu
+
+
+def ngpus():
+    try:
+        import torch
+
+        return torch.cuda.device_count()
+    except Exception:
+        return 0
+
+
+def free_port():
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    return p
+
+
+@pytest.mark.parametrize("graph", [False, True])
+def test_dist_check_two_gpus(graph):
+    if ngpus() < 2:
+        pytest.skip("needs 2 GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(REPO, "tools", "dist_check.py"), "--grid", "24"]
+    if graph:
+        cmd.append("--graph")
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 2, p.stdout[-2000:] + p.stderr[-2000:]
+    for rec in lines:
+        assert rec["ok"], rec
+    assert p.returncode == 0

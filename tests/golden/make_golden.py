@@ -261,8 +261,23 @@ def hashes():
     print("wrote", path)
 
 
+def cli_reports():
+    """Reference `amgpoly solve` JSON reports (cli.py:193-255) for small runs."""
+    from amgpoly.cli import main as cli_main
+
+    for name, overrides in {
+        "cli_solve_m8_matching.json": ["m=8", "coarsening=pairwise_matching"],
+        "cli_solve_m12_sa.json": ["m=12", "smoother=cheb4", "tol=1e-6"],
+        "cli_solve_m6_itmax1.json": ["m=6", "itmax=1"],
+    }.items():
+        args = ["solve"] + [x for o in overrides for x in ("--override", o)]
+        cli_main(args + ["-o", os.path.join(HERE, name)])
+        print("wrote", name)
+
+
 if __name__ == "__main__":
     export_params()
     smoother_small()
     hier_small()
     hashes()
+    cli_reports()

@@ -1,0 +1,101 @@
+#!/usr/bin/env python
+"""Per-level cost of halo exchanges in the distributed hierarchy (torchrun).
+
+For every distributed matrix of the rank (A_l, P_l, R_l) times amgp_spmv
+with its halo plan (NCCL exchange overlapped with interior rows) against the
+same local matrix without a plan (operand already extended: no
+communication), and the exchange alone.
+
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/dist_levels.py --grid 161
+"""
+
+import argparse
+import json
+import os
+import sys
+
+REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, REPO)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--grid", type=int, default=161)
+    ap.add_argument("--reps", type=int, default=50)
+    ap.add_argument("--replicate-below", type=int, default=20000)
+    args = ap.parse_args()
+    import torch
+    import torch.distributed as dist
+
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dist.init_process_group("gloo")
+    import paper_2407_09848_b200 as P
+    from paper_2407_09848_b200 import _native as N
+    from paper_2407_09848_b200 import dist as D
+    from paper_2407_09848_b200.sparse import DeviceMatrix
+
+    comm = D.Communicator(local)
+    c = comm.ctx
+    cfg = P.PolySmootherConfig(family="opt_cheb4", degree=4)
+
+    def build():
+        A, _ = P.poisson3d(args.grid)
+        return P.build_hierarchy(A, smoother=cfg)
+
+    d, path = D.share_hierarchy(build, comm.rank, dist.barrier)
+    L = int(d["nlev"][0])
+    A_glob = [D._mat(d, f"A{l}") for l in range(L)]
+
+    class _H:
+        levels = [type("Lv", (), {"A": a}) for a in A_glob]
+
+    parts = D.level_partitions(_H, comm.size, args.replicate_below)
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        dist.barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(c.stream)
+        for _ in range(args.reps):
+            fn()
+        e1.record(c.stream)
+        torch.cuda.synchronize()
+        return round(e0.elapsed_time(e1) / args.reps * 1e3, 2)
+
+    rows = []
+    for l in range(L):
+        mats = [("A", A_glob[l], parts[l], parts[l])]
+        if l < L - 1:
+            mats += [("P", D._mat(d, f"P{l}"), parts[l], parts[l + 1]),
+                     ("R", D._mat(d, f"R{l}"), parts[l + 1], parts[l])]
+        for name, M, roff, coff in mats:
+            Ml, plan = D.localize(M, roff, coff, comm.rank)
+            Dh = D.attach_halo(DeviceMatrix.from_csr(Ml, c), plan)
+            Dn = DeviceMatrix.from_csr(Ml, c)
+            nown = plan.nown if plan is not None else Ml.ncols
+            x = torch.randn(Ml.ncols, dtype=torch.float64, device="cuda")
+            y = torch.empty(Ml.nrows, dtype=torch.float64, device="cuda")
+
+            def run(Dm):
+                def f():
+                    with c.scope():
+                        N.check(N.lib().amgp_spmv(c.handle, Dm.handle, N.ptr(x), N.ptr(y)))
+                return f
+
+            rec = {"level": l, "mat": name, "rows": Ml.nrows, "nnz": Ml.nnz,
+                   "halo": plan.nhalo if plan is not None else 0,
+                   "peers": len(plan.peers) if plan is not None else 0,
+                   "us_halo": timed(run(Dh)), "us_local": timed(run(Dn))}
+            rows.append(rec)
+    if comm.rank == 0:
+        for r in rows:
+            print(json.dumps(r), flush=True)
+        os.unlink(path)
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -34,8 +34,9 @@ extern "C" {
 /* smoothers.py:28 FAMILIES */
 enum { AMGP_L1_JACOBI = 0, AMGP_CHEB4 = 1, AMGP_OPT_CHEB4 = 2, AMGP_OPT_CHEB1 = 3 };
 
-/* krylov.py:15-26 KrylovConfig.variant */
-enum { AMGP_PCG = 0, AMGP_FCG = 1 };
+/* krylov.py:15-26 KrylovConfig.variant; AMGP_PCG1 = single-reduction PCG
+ * (Chronopoulos-Gear; one global reduction per iteration) */
+enum { AMGP_PCG = 0, AMGP_FCG = 1, AMGP_PCG1 = 2 };
 
 /* amg.py:65 AmgHierarchy.coarse_solver; AMGP_COARSE_SMOOTHER applies the
  * coarsest level's own smoother from a zero guess, which turns a one-level

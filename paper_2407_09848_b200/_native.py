@@ -26,6 +26,7 @@ AMGP_EINVAL = -1
 
 FAMILY_CODES = {"l1_jacobi": 0, "cheb4": 1, "opt_cheb4": 2, "opt_cheb1": 3}
 COARSE_CODES = {"l1_jacobi": 0, "dense_direct": 1, "smoother": 2}
+VARIANT_CODES = {"pcg": 0, "fcg": 1, "pcg1": 2}
 
 _P64 = C.POINTER(C.c_int64)
 _PD = C.POINTER(C.c_double)

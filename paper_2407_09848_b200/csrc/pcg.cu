@@ -37,7 +37,7 @@ enum {
 };
 
 // what the folded totals of a reduction become (krylov.py line numbers)
-enum { OP_BNORM, OP_RELRES, OP_RZ, OP_DAD, OP_DAD_FCG, OP_BETA, OP_BETA_FCG };
+enum { OP_BNORM, OP_RELRES, OP_RZ, OP_DAD, OP_DAD_FCG, OP_BETA, OP_BETA_FCG, OP_CG1 };
 
 #define RB 256          // reduction block
 #define RGRID_MAX 1184  // 148 SMs x 8
@@ -70,6 +70,21 @@ __device__ __forceinline__ void apply_op(int op, const double *t, double *sc) {
         case OP_BETA_FCG:  // :118
             sc[S_BETA] = __ddiv_rn(t[0], sc[S_DAD]);
             break;
+        case OP_CG1: {  // single-reduction PCG: t = (r.u, w.u, r.r), u = M r, w = A u
+            const double g = t[0], dl = t[1];
+            sc[S_RELRES] = __ddiv_rn(sqrt(t[2]), sc[S_BNORM]);
+            double beta = 0.0, denom = dl;
+            if (sc[S_AUX] != 0.0) {
+                beta = __ddiv_rn(g, sc[S_RZ]);
+                denom = __dsub_rn(dl, __ddiv_rn(__dmul_rn(beta, g), sc[S_ALPHA]));
+            }
+            if (denom <= 0.0) sc[S_BRK] = 1.0;  // p.Ap <= 0 (krylov.py:97-99 analogue)
+            sc[S_BETA] = beta;
+            sc[S_ALPHA] = __ddiv_rn(g, denom);
+            sc[S_RZ] = g;
+            sc[S_AUX] = 1.0;
+            break;
+        }
     }
 }
 
@@ -180,6 +195,36 @@ k_pcg_update(int64_t n, double *__restrict__ x, double *__restrict__ r,
     reduce_finish<1>(acc, partial, ticket, OP_RELRES, dist, sc);
 }
 
+// (r.u, w.u, r.r) in one pass -- the single reduction of the pcg1 variant
+__global__ void __launch_bounds__(RB)
+k_cg1_dot3(int64_t n, const double *__restrict__ r, const double *__restrict__ u,
+           const double *__restrict__ w, double *partial, unsigned *ticket, double *sc, int dist) {
+    double acc[3] = {0.0, 0.0, 0.0};
+    for (int64_t i = (int64_t)blockIdx.x * RB + threadIdx.x; i < n; i += (int64_t)gridDim.x * RB) {
+        const double ri = r[i], ui = u[i];
+        acc[0] = __dadd_rn(acc[0], __dmul_rn(ri, ui));
+        acc[1] = __dadd_rn(acc[1], __dmul_rn(w[i], ui));
+        acc[2] = __dadd_rn(acc[2], __dmul_rn(ri, ri));
+    }
+    reduce_finish<3>(acc, partial, ticket, OP_CG1, dist, sc);
+}
+
+// p = u + beta p ; s = w + beta s ; x += alpha p ; r -= alpha s
+__global__ void k_cg1_update(int64_t n, const double *__restrict__ u, const double *__restrict__ w,
+                             double *__restrict__ p, double *__restrict__ s, double *__restrict__ x,
+                             double *__restrict__ r, const double *sc) {
+    const double alpha = sc[S_ALPHA], beta = sc[S_BETA];
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const double pi = __dadd_rn(u[i], __dmul_rn(beta, p[i]));
+        const double si = __dadd_rn(w[i], __dmul_rn(beta, s[i]));
+        p[i] = pi;
+        s[i] = si;
+        x[i] = __dadd_rn(x[i], __dmul_rn(alpha, pi));
+        r[i] = __dsub_rn(r[i], __dmul_rn(alpha, si));
+    }
+}
+
 template <bool FCG>
 __global__ void k_pcg_dir(int64_t n, const double *__restrict__ z, double *__restrict__ d,
                           const double *sc) {
@@ -202,13 +247,13 @@ namespace {
 struct PcgWork {  // views into the context's cached PCG workspace
     double *partial = nullptr;
     unsigned *ticket = nullptr;
-    double *r = nullptr, *z = nullptr, *d = nullptr, *Ad = nullptr;
+    double *r = nullptr, *z = nullptr, *d = nullptr, *Ad = nullptr, *s = nullptr;
 };
 
 // Grow-only workspace cached on the context: cudaMalloc/cudaFree per solve
 // would synchronise the device inside the caller's pipeline.
 int pcg_workspace(amgp_ctx *ctx, int64_t n, PcgWork *w) {
-    const int64_t need = 4 * std::max<int64_t>(n, 1) + 2 * RGRID_MAX + 8;
+    const int64_t need = 5 * std::max<int64_t>(n, 1) + 3 * RGRID_MAX + 8;
     if (ctx->red_partial_n < need) {
         cudaStreamSynchronize(ctx->stream);
         cudaFree(ctx->red_partial);
@@ -222,10 +267,11 @@ int pcg_workspace(amgp_ctx *ctx, int64_t n, PcgWork *w) {
     const int64_t nn = std::max<int64_t>(n, 1);
     w->ticket = (unsigned *)p;  // 8 doubles of room for the tickets (zeroed once)
     w->partial = p + 8;
-    w->r = w->partial + 2 * RGRID_MAX;
+    w->r = w->partial + 3 * RGRID_MAX;
     w->z = w->r + nn;
     w->d = w->z + nn;
     w->Ad = w->d + nn;
+    w->s = w->Ad + nn;
     return AMGP_OK;
 }
 }  // namespace
@@ -238,7 +284,7 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
                               double *x, int x0_given, int variant, double tol, int itmax,
                               double *history, amgp_solve_report *rep) {
     if (!ctx || !A || !rep) return amgp_fail(AMGP_EINVAL, "amgp_pcg_solve: bad argument");
-    if (variant != AMGP_PCG && variant != AMGP_FCG)
+    if (variant != AMGP_PCG && variant != AMGP_FCG && variant != AMGP_PCG1)
         return amgp_fail(AMGP_EINVAL, "unknown Krylov variant");
     if (!(tol > 0.0) || itmax < 1) return amgp_fail(AMGP_EINVAL, "tol must be positive and itmax >= 1");
     const int64_t nown = A->halo ? A->halo->nown : A->ncols;
@@ -318,6 +364,46 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
         return AMGP_OK;
     };
     if (relres <= tol) return finish(0, true, false);
+
+    if (variant == AMGP_PCG1) {
+        // Chronopoulos-Gear single-reduction PCG (the paper's "CG requiring
+        // only one global synchronization"): per iteration
+        // u = M r, w = A u and ONE fused reduction (r.u, w.u, r.r); the
+        // residual norm of the current iterate arrives with it, so a
+        // converged solve costs one extra preconditioner application.
+        std::unique_lock<std::mutex> hl1;
+        if (h) hl1 = std::unique_lock<std::mutex>(hier_mutex(h));
+        double *u = w.z, *ww = w.Ad, *pp = w.d, *ss = w.s;
+        AMGP_CUDA(cudaMemsetAsync(sc + S_AUX, 0, sizeof(double), st));
+        AMGP_CUDA(cudaMemsetAsync(sc + S_BRK, 0, sizeof(double), st));
+        AMGP_CUDA(cudaMemsetAsync(pp, 0, nb, st));
+        AMGP_CUDA(cudaMemsetAsync(ss, 0, nb, st));
+        for (int it = 0;; it++) {
+            if (h) AMGP_TRY(vcycle_enqueue(h, w.r, u));
+            else AMGP_CUDA(cudaMemcpyAsync(u, w.r, nb, cudaMemcpyDeviceToDevice, st));
+            pc++;
+            AMGP_TRY(spmv_enqueue(ctx, A, u, ww));
+            spmv++;
+            k_cg1_dot3<<<g, RB, 0, st>>>(n, w.r, u, ww, w.partial, w.ticket, sc, dist);
+            AMGP_CHECK_LAUNCH(ctx);
+            if (dist) {
+                AMGP_TRY(allreduce_sum_ordered(ctx, sc + S_LOC, 3, sc + S_GLB));
+                k_apply_op<<<1, 1, 0, st>>>(OP_CG1, sc);
+                AMGP_CHECK_LAUNCH(ctx);
+            }
+            AMGP_TRY(fetch());
+            if (it > 0) {
+                relres = hs[S_RELRES];
+                if (history) history[nh] = relres;
+                nh++;
+                if (relres <= tol) return finish(it, true, false);
+            }
+            if (hs[S_BRK] != 0.0) return finish(it, false, true);
+            if (it == itmax) return finish(itmax, false, false);
+            k_cg1_update<<<g, RB, 0, st>>>(n, u, ww, pp, ss, x, w.r, sc);
+            AMGP_CHECK_LAUNCH(ctx);
+        }
+    }
 
     std::unique_lock<std::mutex> hl;
     if (h) hl = std::unique_lock<std::mutex>(hier_mutex(h));

@@ -320,7 +320,7 @@ class DistHierarchy:
             x = N.to_device(x0, c, copy=True) if x0 is not None else N.empty(self.n_local, c)
             N.check(N.lib().amgp_pcg_solve(
                 c.handle, self.As[0].handle, self.handle, N.ptr(bd), N.ptr(x), int(x0 is not None),
-                0 if cfg.variant == "pcg" else 1, float(cfg.tol), int(cfg.itmax),
+                N.VARIANT_CODES[cfg.variant], float(cfg.tol), int(cfg.itmax),
                 hist.ctypes.data_as(N._PD) if hist is not None else None, C.byref(rep)))
         report = SolveReport(iterations=rep.iterations, converged=bool(rep.converged),
                              final_relres=rep.final_relres,

@@ -29,7 +29,7 @@ class KrylovConfig:
     record_history: bool = True
 
     def __post_init__(self):
-        if self.variant not in ("pcg", "fcg"):
+        if self.variant not in N.VARIANT_CODES:  # pcg | fcg | pcg1 (single reduction)
             raise ValueError(f"unknown Krylov variant {self.variant!r}")
         if self.tol <= 0.0 or self.itmax < 1:
             raise ValueError("tol must be positive and itmax >= 1")
@@ -81,7 +81,7 @@ def solve(A, b, precond=None, cfg=None, x0=None):
         x = N.to_device(x0, c, copy=True) if x0 is not None else N.empty(n, c)
         N.check(N.lib().amgp_pcg_solve(
             c.handle, D.handle, H.handle if H is not None else None, N.ptr(bd), N.ptr(x),
-            int(x0 is not None), 0 if cfg.variant == "pcg" else 1, float(cfg.tol), int(cfg.itmax),
+            int(x0 is not None), N.VARIANT_CODES[cfg.variant], float(cfg.tol), int(cfg.itmax),
             hist.ctypes.data_as(N._PD) if hist is not None else None, C.byref(rep)))
     report = SolveReport(
         iterations=rep.iterations,

@@ -407,3 +407,31 @@ def test_smoother_digests_32cube_all_levels(P):
         for fam in FAMILIES:
             cfg = P.PolySmootherConfig(family=fam, degree=4)
             assert _sha(P.smoother_apply(cfg, Al, Ml, bl, xl)) == ref["smoother"][f"L{l}_{fam}_k4_x0"]
+
+
+@pytest.mark.parametrize("kind", ["smoothed_aggregation", "pairwise_matching"])
+def test_single_reduction_pcg_iterations(P, kind):
+    """pcg1 (Chronopoulos-Gear, one global reduction per iteration) is
+    mathematically PCG: iteration counts within +-1 of the reference's."""
+    ref = golden("hashes.json")[f"p3d32_{kind}"]
+    A, b = P.poisson3d(32)
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+                          smoother=P.PolySmootherConfig(family="cheb4", degree=4))
+    Ad = A.to_scipy()
+    for fam in FAMILIES:
+        for k in (1, 4, 6):
+            cfg = P.PolySmootherConfig(family=fam, degree=k)
+            for lv in h.levels:
+                lv.smoother = cfg
+            x, rep = P.solve(A, b, precond=P.as_vcycle_preconditioner(h),
+                             cfg=P.KrylovConfig(tol=1e-6, variant="pcg1"))
+            want = ref["pcg"][f"{fam}_k{k}"]["iterations"]
+            assert rep.converged and abs(rep.iterations - want) <= 1, (fam, k, rep.iterations, want)
+            relres = np.linalg.norm(b - Ad @ x) / np.linalg.norm(b)
+            assert relres <= 1.01e-6
+            assert rep.residual_history[-1] == rep.final_relres
+    # plain CG (no preconditioner) on a small SPD system
+    T = P.CsrMatrix.from_dense(2 * np.eye(40) - np.eye(40, k=1) - np.eye(40, k=-1))
+    x, rep = P.solve(T, np.ones(40), cfg=P.KrylovConfig(tol=1e-10, itmax=200, variant="pcg1"))
+    assert rep.converged
+    assert np.linalg.norm(np.ones(40) - T.to_dense() @ x) / np.sqrt(40) <= 1e-9

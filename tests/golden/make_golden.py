@@ -261,6 +261,47 @@ def hashes():
     print("wrote", path)
 
 
+def stencil27():
+    """27-point Poisson (BASELINE configs[4]; not in the reference): the input
+    matrix comes from this repo's numpy generator (problems.poisson3d_27, a
+    pure data generator), everything else -- hierarchy, V-cycle, PCG -- from
+    the reference."""
+    sys.path.insert(0, REPO)
+    from paper_2407_09848_b200.problems import poisson3d_27
+
+    doc = {}
+    for m in (12, 20):
+        B, b = poisson3d_27(m)
+        A = CsrMatrix(B.nrows, B.ncols, B.row_ptr, B.col_idx, B.values)
+        rec = {}
+        for kind in ("smoothed_aggregation", "pairwise_matching"):
+            h = build_hierarchy(A, coarsening=CoarseningConfig(kind=kind),
+                                smoother=PolySmootherConfig(family="opt_cheb1", degree=3))
+            r = {"levels": []}
+            for lev in h.levels:
+                lr = {"A": mat_digest(lev.A), "M": sha(lev.M.m_diag, "f")}
+                if lev.P is not None:
+                    lr["P"] = mat_digest(lev.P)
+                    lr["R"] = mat_digest(lev.restrict_op())
+                r["levels"].append(lr)
+            rr = np.random.default_rng(5).standard_normal(A.nrows)
+            r["vcycle_opt_cheb1_k3"] = sha(vcycle_apply(h, rr), "f")
+            r["pcg"] = {}
+            for fam in FAMILIES:
+                set_smoother(h, PolySmootherConfig(family=fam, degree=3))
+                _, rep = solve(A, b, precond=as_vcycle_preconditioner(h),
+                               cfg=KrylovConfig(tol=1e-6, itmax=1000))
+                r["pcg"][f"{fam}_k3"] = {"iterations": rep.iterations,
+                                         "final_relres": rep.final_relres}
+            rec[kind] = r
+        doc[f"p27_{m}"] = rec
+        print("27-point", m, {k: v["pcg"]["opt_cheb1_k3"]["iterations"] for k, v in rec.items()})
+    path = os.path.join(HERE, "hashes27.json")
+    with open(path, "w") as f:
+        json.dump(doc, f, indent=1)
+    print("wrote", path)
+
+
 def cli_reports():
     """Reference `amgpoly solve` JSON reports (cli.py:193-255) for small runs."""
     from amgpoly.cli import main as cli_main
@@ -280,4 +321,5 @@ if __name__ == "__main__":
     smoother_small()
     hier_small()
     hashes()
+    stencil27()
     cli_reports()

@@ -409,6 +409,25 @@ def test_smoother_digests_32cube_all_levels(P):
             assert _sha(P.smoother_apply(cfg, Al, Ml, bl, xl)) == ref["smoother"][f"L{l}_{fam}_k4_x0"]
 
 
+@pytest.mark.parametrize("m", [12, 20])
+@pytest.mark.parametrize("kind", ["smoothed_aggregation", "pairwise_matching"])
+def test_27point_vcycle_digest_and_pcg_table(P, m, kind):
+    """27-point Poisson (configs[4] stencil): device V-cycle bitwise equal to the
+    reference's on the same hierarchy; PCG iterations equal the reference's."""
+    ref = golden("hashes27.json")[f"p27_{m}"][kind]
+    A, b = P.poisson3d_27(m)
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+                          smoother=P.PolySmootherConfig(family="opt_cheb1", degree=3))
+    r = np.random.default_rng(5).standard_normal(A.nrows)
+    assert _sha(P.vcycle_apply(h, r)) == ref["vcycle_opt_cheb1_k3"]
+    for fam in FAMILIES:
+        cfg = P.PolySmootherConfig(family=fam, degree=3)
+        for lv in h.levels:
+            lv.smoother = cfg
+        _, rep = P.solve(A, b, precond=P.as_vcycle_preconditioner(h), cfg=P.KrylovConfig(tol=1e-6))
+        assert rep.converged and rep.iterations == ref["pcg"][f"{fam}_k3"]["iterations"], fam
+
+
 @pytest.mark.parametrize("kind", ["smoothed_aggregation", "pairwise_matching"])
 def test_single_reduction_pcg_iterations(P, kind):
     """pcg1 (Chronopoulos-Gear, one global reduction per iteration) is

@@ -70,6 +70,23 @@ def test_hierarchy_digests(m, kind):
             assert mat_digest(lv.restrict_op()) == lr["R"], (m, kind, l, "R")
 
 
+@pytest.mark.parametrize("m", [12, 20])
+@pytest.mark.parametrize("kind", ["smoothed_aggregation", "pairwise_matching"])
+def test_hierarchy_digests_27point(m, kind):
+    """27-point stencil (BASELINE configs[4]): native setup == reference setup."""
+    ref = golden("hashes27.json")[f"p27_{m}"][kind]
+    A, _ = P.poisson3d_27(m)
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+                          smoother=P.PolySmootherConfig(family="opt_cheb1", degree=3))
+    assert len(h.levels) == len(ref["levels"])
+    for l, (lv, lr) in enumerate(zip(h.levels, ref["levels"])):
+        assert mat_digest(lv.A) == lr["A"], (m, kind, l, "A")
+        assert sha(lv.M.m_diag, "f") == lr["M"], (m, kind, l, "M")
+        if "P" in lr:
+            assert mat_digest(lv.P) == lr["P"], (m, kind, l, "P")
+            assert mat_digest(lv.restrict_op()) == lr["R"], (m, kind, l, "R")
+
+
 def test_aggregation_unit_cases():
     # tests/test_amg.py:25-68 of the reference
     Pm = S.sa_aggregate(P.CsrMatrix.identity(5))

@@ -84,6 +84,8 @@ _SIGS = {
     "amgp_hier_set_smoother": (C.c_int, [_VP, C.c_int, C.POINTER(SmootherCfg)]),
     "amgp_hier_set_coarse_cholesky": (C.c_int, [_VP, _PD]),
     "amgp_hier_use_graph": (C.c_int, [_VP, C.c_int]),
+    "amgp_hier_use_tail": (C.c_int, [_VP, C.c_int]),
+    "amgp_hier_info": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
     "amgp_hier_destroy": (C.c_int, [_VP]),
     "amgp_vcycle_apply": (C.c_int, [_VP, _VP, _VP]),
     "amgp_pcg_solve": (C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, C.c_int, C.c_double, C.c_int,

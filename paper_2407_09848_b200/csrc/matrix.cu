@@ -13,7 +13,7 @@
 #include <algorithm>
 #include <vector>
 
-#include "rows.cuh"
+#include "epilogues.cuh"
 
 // ---------------------------------------------------------------- host packing
 extern "C" int amgp_sell_pack_host(int64_t nrows, const int64_t *row_ptr,
@@ -393,19 +393,6 @@ extern "C" int amgp_mat_l1_diag(amgp_mat *A, double *m_dev) {
 }
 
 // ---------------------------------------------------------------- SpMV kernels
-// MODE 0: y = A x ; MODE 1: y = r - A x (amg.py:311) ; MODE 2: y = y + A x (amg.py:314)
-template <int MODE>
-struct SpmvEpi {
-    static constexpr bool kSpmv = true;
-    const double *__restrict__ r;
-    double *y;
-    __device__ __forceinline__ void operator()(int64_t row, double sum) const {
-        if (MODE == 0) y[row] = sum;
-        else if (MODE == 1) y[row] = __dsub_rn(r[row], sum);
-        else y[row] = __dadd_rn(y[row], sum);
-    }
-};
-
 int spmv_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y) {
     return launch_rows(ctx, A, x, SpmvEpi<0>{nullptr, y});
 }

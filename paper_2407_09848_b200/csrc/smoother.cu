@@ -19,76 +19,7 @@
 // With x0 == 0 the first SpMV is skipped (b - A*0 == b bitwise).
 #include <algorithm>
 
-#include "rows.cuh"
-
-// ---------------------------------------------------------------- epilogues
-template <bool FIRST, bool LAST, bool X0>
-struct Cheb4Step {
-    static constexpr bool kSpmv = !FIRST || X0;
-    const double *__restrict__ m;
-    const double *__restrict__ b;
-    const double *__restrict__ xg;  // x0 (first step) or z_{j-1}
-    double *__restrict__ r;
-    double *__restrict__ znew;
-    double *__restrict__ x;
-    double cz, cr, beta;
-    __device__ __forceinline__ void operator()(int64_t row, double y) const {
-        const double rr = __dsub_rn(FIRST ? b[row] : r[row], y);
-        double z = FIRST ? __dmul_rn(0.0, cz) : __dmul_rn(xg[row], cz);
-        z = __dadd_rn(z, __dmul_rn(cr, __ddiv_rn(rr, m[row])));
-        const double xo = FIRST ? (X0 ? xg[row] : 0.0) : x[row];
-        x[row] = __dadd_rn(xo, __dmul_rn(beta, z));
-        if (!LAST) {
-            r[row] = rr;
-            znew[row] = z;
-        }
-    }
-};
-
-template <bool FIRST, bool LAST, bool X0, bool RHO1>
-struct Cheb1Step {
-    static constexpr bool kSpmv = !FIRST || X0;
-    const double *__restrict__ m;
-    const double *__restrict__ b;
-    const double *__restrict__ xg;  // x0 (init) or d_{j-1}
-    double *__restrict__ r;
-    double *__restrict__ dnew;
-    double *__restrict__ x;
-    double c0, c1, rho;  // init: c0 = theta; step: c0 = rho_j rho_{j-1}, c1 = 2 rho_j / delta
-    __device__ __forceinline__ void operator()(int64_t row, double y) const {
-        double rr, d, xo;
-        if (FIRST) {
-            rr = __ddiv_rn(__dsub_rn(b[row], y), m[row]);
-            if (!RHO1) rr = __ddiv_rn(rr, rho);
-            d = __ddiv_rn(rr, c0);
-            xo = X0 ? xg[row] : 0.0;
-        } else {
-            double sv = __ddiv_rn(y, m[row]);
-            if (!RHO1) sv = __ddiv_rn(sv, rho);
-            rr = __dsub_rn(r[row], sv);
-            d = __dadd_rn(__dmul_rn(xg[row], c0), __dmul_rn(c1, rr));
-            xo = x[row];
-        }
-        x[row] = __dadd_rn(xo, d);
-        if (!LAST) {
-            r[row] = rr;
-            dnew[row] = d;
-        }
-    }
-};
-
-template <bool X0>
-struct L1Sweep {
-    static constexpr bool kSpmv = X0;
-    const double *__restrict__ m;
-    const double *__restrict__ b;
-    const double *__restrict__ xin;
-    double *__restrict__ xout;
-    __device__ __forceinline__ void operator()(int64_t row, double y) const {
-        const double rr = __dsub_rn(b[row], y);
-        xout[row] = __dadd_rn(X0 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
-    }
-};
+#include "epilogues.cuh"
 
 // sparse.py:128-139 fused_update (elementwise, in place)
 __global__ void k_fused_update(int64_t n, double rp, double c, const double *__restrict__ s,

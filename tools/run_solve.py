@@ -21,6 +21,7 @@ def main():
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--no-graph", action="store_true")
+    ap.add_argument("--no-tail", action="store_true")
     args = ap.parse_args()
     import torch
 
@@ -34,14 +35,16 @@ def main():
     setup = time.perf_counter() - t0
     D = h.device()
     if args.no_graph:
-        N.check(N.lib().amgp_hier_use_graph(D.handle, 0))
+        D.use_graph(False)
+    if args.no_tail:
+        D.use_tail(False)
     bd = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
     for i in range(args.repeat):
         x, rep = P.solve(A, bd, precond=P.as_vcycle_preconditioner(h), cfg=P.KrylovConfig(tol=1e-6))
         torch.cuda.synchronize()
         print(f"m={args.m} {args.kind} {args.family} k={args.k}: setup {setup:.2f}s "
               f"iters {rep.iterations} relres {rep.final_relres:.3e} solve {rep.elapsed_s * 1e3:.2f} ms "
-              f"levels {[lv.A.nrows for lv in h.levels]}", flush=True)
+              f"levels {[lv.A.nrows for lv in h.levels]} tail_start {D.tail_start()}", flush=True)
 
 
 if __name__ == "__main__":

@@ -42,6 +42,7 @@ struct TailLev {
     const double *r;   // rhs (levels >= 1 of the tail; level 0 comes as a kernel argument)
     double *z, *xpre, *res, *work;
     int64_t n;
+    int wA, wP, wR;  // widest slice of A, P, R (picks the phase schedule)
     int family, degree;
     double rho;
     double coef[3 * TAIL_MAX_K];
@@ -189,24 +190,65 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
 }
 
 // ---------------------------------------------------------------- K8 device side
+// One grid-wide phase: y = A xg row by row, then epi(row, y).  Short rows
+// (the matrix's widest slice <= TAIL_SHORT slots): every thread of the grid
+// owns rows (a warp = one slice) and sums its slots in order.  Long rows: a
+// CTA owns a slice, its warps form the slot products (8 independent loads in
+// flight per thread) into shared memory, warp 0 sums them in slot order.
+// Operands written by earlier phases are read with ld.global.cg (L2), never
+// through the non-coherent path.
+#define TAIL_SHORT 16
 template <class Epi>
-__device__ void tail_phase(const SellView &A, const double *xg, const Epi &epi, double *prod) {
+__device__ void tail_phase(const SellView &A, int wmax, const double *xg, const Epi &epi,
+                           double *prod) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    if (!Epi::kSpmv || wmax <= TAIL_SHORT) {
+        const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
+        for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.nslices * 32;
+             row += nthr) {
+            double y = 0.0;
+            if (Epi::kSpmv) {
+                const int64_t s = row >> 5, base = __ldg(A.slice_ptr + s);
+                const int w = (int)((__ldg(A.slice_ptr + s + 1) - base) >> 5);
+                const int32_t *cp = A.col + base + (row & 31);
+                const double *vp = A.val + base + (row & 31);
+                int32_t cc[TAIL_SHORT];
+                double pv[TAIL_SHORT];
+#pragma unroll
+                for (int j = 0; j < TAIL_SHORT; j++) cc[j] = j < w ? __ldg(cp + j * 32) : -1;
+#pragma unroll
+                for (int j = 0; j < TAIL_SHORT; j++)
+                    pv[j] = cc[j] >= 0 ? __dmul_rn(__ldg(vp + j * 32), __ldcg(xg + cc[j])) : 0.0;
+#pragma unroll
+                for (int j = 0; j < TAIL_SHORT; j++)
+                    if (cc[j] >= 0) y = __dadd_rn(y, pv[j]);
+            }
+            if (row < A.nrows) epi(row, y);
+        }
+        return;
+    }
+    constexpr int NW = TAIL_THREADS / 32;
     for (int64_t s = blockIdx.x; s < A.nslices; s += gridDim.x) {
         const int64_t row = s * 32 + lane;
-        if (!Epi::kSpmv) {
-            if (warp == 0 && row < A.nrows) epi(row, 0.0);
-            continue;
-        }
-        const int64_t base = A.slice_ptr[s];
-        const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
+        const int64_t base = __ldg(A.slice_ptr + s);
+        const int w = (int)((__ldg(A.slice_ptr + s + 1) - base) >> 5);
         double sum = 0.0;
         for (int j0 = 0; j0 < w; j0 += TAIL_CHUNK) {
             const int jn = min(TAIL_CHUNK, w - j0);
-            for (int j = warp; j < jn; j += TAIL_THREADS / 32) {
-                const int64_t o = base + (int64_t)(j0 + j) * 32 + lane;
-                const int32_t c = __ldg(A.col + o);
-                prod[j * 32 + lane] = c >= 0 ? __dmul_rn(__ldg(A.val + o), __ldcg(xg + c)) : 0.0;
+            for (int j = warp; j < jn; j += NW * 8) {
+                int32_t cc[8];
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int jj = j + u * NW;
+                    cc[u] = jj < jn ? __ldg(A.col + base + (int64_t)(j0 + jj) * 32 + lane) : -2;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; u++) {
+                    const int jj = j + u * NW;
+                    if (cc[u] == -2) continue;
+                    const double v = __ldg(A.val + base + (int64_t)(j0 + jj) * 32 + lane);
+                    prod[jj * 32 + lane] = cc[u] >= 0 ? __dmul_rn(v, __ldcg(xg + cc[u])) : 0.0;
+                }
             }
             __syncthreads();
             if (warp == 0)
@@ -221,7 +263,7 @@ template <bool FIRST, bool LAST, bool X0>
 __device__ __forceinline__ void tail_cheb4(const TailLev &L, const double *b, const double *xg,
                                            double *r, double *zn, double *x, int j, double *prod) {
     const double *c = L.coef + 3 * (j - 1);
-    tail_phase(L.A, xg, Cheb4Step<FIRST, LAST, X0>{L.m, b, xg, r, zn, x, c[0], c[1], c[2]}, prod);
+    tail_phase(L.A, L.wA, xg, Cheb4Step<FIRST, LAST, X0>{L.m, b, xg, r, zn, x, c[0], c[1], c[2]}, prod);
 }
 
 template <bool FIRST, bool LAST, bool X0>
@@ -230,9 +272,9 @@ __device__ __forceinline__ void tail_cheb1(const TailLev &L, const double *b, co
     const double c0 = j == 0 ? L.coef[0] : L.coef[1 + 2 * (j - 1)];
     const double c1 = j == 0 ? 0.0 : L.coef[2 + 2 * (j - 1)];
     if (L.rho == 1.0)
-        tail_phase(L.A, xg, Cheb1Step<FIRST, LAST, X0, true>{L.m, b, xg, r, dn, x, c0, c1, L.rho}, prod);
+        tail_phase(L.A, L.wA, xg, Cheb1Step<FIRST, LAST, X0, true>{L.m, b, xg, r, dn, x, c0, c1, L.rho}, prod);
     else
-        tail_phase(L.A, xg, Cheb1Step<FIRST, LAST, X0, false>{L.m, b, xg, r, dn, x, c0, c1, L.rho}, prod);
+        tail_phase(L.A, L.wA, xg, Cheb1Step<FIRST, LAST, X0, false>{L.m, b, xg, r, dn, x, c0, c1, L.rho}, prod);
 }
 
 // smoother_enqueue (smoother.cu) as grid-wide phases, same buffers and order
@@ -246,8 +288,8 @@ __device__ void tail_smoother(const TailLev &L, const double *b, const double *x
         const double *xin = x0;
         for (int s = 1; s <= k; s++) {
             double *xout = ((k - s) % 2 == 0) ? x : tmp;
-            if (s == 1 && !hx0) tail_phase(L.A, nullptr, L1Sweep<false>{L.m, b, nullptr, xout}, prod);
-            else tail_phase(L.A, xin, L1Sweep<true>{L.m, b, xin, xout}, prod);
+            if (s == 1 && !hx0) tail_phase(L.A, L.wA, nullptr, L1Sweep<false>{L.m, b, nullptr, xout}, prod);
+            else tail_phase(L.A, L.wA, xin, L1Sweep<true>{L.m, b, xin, xout}, prod);
             grid.sync();
             xin = xout;
         }
@@ -344,9 +386,9 @@ k_vcycle_tail(const TailDesc *__restrict__ D, const double *r0, double *z0) {
         const TailLev &V = D->lev[t];
         const double *r = t == 0 ? r0 : V.r;
         tail_smoother(V, r, nullptr, V.xpre, smem, grid);
-        tail_phase(V.A, V.xpre, SpmvEpi<1>{r, V.res}, smem);
+        tail_phase(V.A, V.wA, V.xpre, SpmvEpi<1>{r, V.res}, smem);
         grid.sync();
-        tail_phase(V.R, V.res, SpmvEpi<0>{nullptr, (double *)D->lev[t + 1].r}, smem);
+        tail_phase(V.R, V.wR, V.res, SpmvEpi<0>{nullptr, (double *)D->lev[t + 1].r}, smem);
         grid.sync();
     }
     {  // coarsest: amg.py:299-300
@@ -357,7 +399,7 @@ k_vcycle_tail(const TailDesc *__restrict__ D, const double *r0, double *z0) {
     for (int t = L - 2; t >= 0; t--) {  // up: amg.py:314-315
         const TailLev &V = D->lev[t];
         const double *r = t == 0 ? r0 : V.r;
-        tail_phase(V.P, D->lev[t + 1].z, SpmvEpi<2>{nullptr, V.xpre}, smem);
+        tail_phase(V.P, V.wP, D->lev[t + 1].z, SpmvEpi<2>{nullptr, V.xpre}, smem);
         grid.sync();
         tail_smoother(V, r, V.xpre, t == 0 ? z0 : V.z, smem, grid);
     }
@@ -395,9 +437,12 @@ static int tail_prepare(amgp_hier *h) {
         const int l = h->tail_start + t;
         TailLev &V = d.lev[t];
         V.A = view_of(h->A[l]);
+        V.wA = h->A[l]->max_width;
         if (l < h->nlev - 1) {
             V.P = view_of(h->P[l]);
             V.R = view_of(h->R[l]);
+            V.wP = h->P[l]->max_width;
+            V.wR = h->R[l]->max_width;
         }
         V.m = h->m[l];
         V.r = h->rl[l];

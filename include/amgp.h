@@ -134,8 +134,8 @@ int amgp_hier_set_smoother(amgp_hier *h, int level, const amgp_smoother_cfg *cfg
 int amgp_hier_set_coarse_cholesky(amgp_hier *h, const double *L_colmajor);
 /* Capture the V-cycle into a CUDA graph on the next apply (1) or not (0). */
 int amgp_hier_use_graph(amgp_hier *h, int enable);
-/* Run the small bottom levels as one cooperative kernel (1, default) or as
- * regular per-step launches (0); identical results either way. */
+/* Run the small bottom levels as one cooperative kernel (1) or as regular
+ * per-step launches (0, default); identical results either way. */
 int amgp_hier_use_tail(amgp_hier *h, int enable);
 /* Levels, and the first level handled by the cooperative tail (-1: none). */
 int amgp_hier_info(amgp_hier *h, int *nlevels, int *tail_start);

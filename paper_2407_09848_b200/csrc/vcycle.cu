@@ -72,7 +72,11 @@ struct amgp_hier {
     double *g_z = nullptr;
     int64_t g_nodes = 0;
     // cooperative tail (K8)
-    bool use_tail = true;
+    // Off by default: measured on B200 (128^3 SA, levels 3-5 in the tail)
+    // 12.4 ms vs 11.6 ms per solve -- the grid barriers plus the sequential
+    // 300-500-term row sums of the coarse SA levels cost more than the
+    // launches they replace (profiles/r01_summary.md).
+    bool use_tail = false;
     bool tail_dirty = true;
     int tail_start = -1;  // first level run by the tail kernel (-1: none)
     TailDesc *d_tail = nullptr;

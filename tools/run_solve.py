@@ -21,7 +21,7 @@ def main():
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--no-tail", action="store_true")
+    ap.add_argument("--tail", action="store_true", help="enable the cooperative V-cycle tail")
     args = ap.parse_args()
     import torch
 
@@ -36,8 +36,8 @@ def main():
     D = h.device()
     if args.no_graph:
         D.use_graph(False)
-    if args.no_tail:
-        D.use_tail(False)
+    if args.tail:
+        D.use_tail(True)
     bd = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
     for i in range(args.repeat):
         x, rep = P.solve(A, bd, precond=P.as_vcycle_preconditioner(h), cfg=P.KrylovConfig(tol=1e-6))

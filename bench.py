@@ -338,7 +338,7 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4):
     dist.barrier()
     if comm.rank == 0:
         try:
-            os.unlink(path)
+            Dist.release_shared(path)
         except OSError:
             pass
     return {"m": m, "n": int(m ** 3), "rows_per_gpu": hi - lo, "family": family, "degree": k,

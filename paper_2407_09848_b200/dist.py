@@ -217,13 +217,42 @@ def poisson3d_block(m, comm, stencil=7):
 
 
 # ---------------------------------------------------------------- hierarchy
+class _SharedArrays:
+    """Mapping key -> array over a directory of .npy files (memory-mapped, so
+    every rank reads only the row blocks it cuts and the page cache is shared)."""
+
+    def __init__(self, path):
+        self.path = path
+        self._cache = {}
+
+    def __getitem__(self, key):
+        if key not in self._cache:
+            self._cache[key] = np.load(os.path.join(self.path, key + ".npy"), mmap_mode="r")
+        return self._cache[key]
+
+    def __contains__(self, key):
+        return os.path.exists(os.path.join(self.path, key + ".npy"))
+
+
 def share_hierarchy(h_or_builder, comm_rank, barrier):
     """Rank 0 builds (callable) or holds the host hierarchy and writes its
-    arrays to /dev/shm; every rank maps them back.  Returns level dicts."""
-    base = os.environ.get("AMGP_SHM", "/dev/shm" if os.path.isdir("/dev/shm") else tempfile.gettempdir())
-    path = os.path.join(base, f"amgp_hier_{os.environ.get('MASTER_PORT', '0')}.npz")
+    arrays as .npy files to /dev/shm (or the temp dir when /dev/shm is too
+    small); every rank memory-maps them.  Returns (arrays, directory)."""
+    import shutil
+
+    name = f"amgp_hier_{os.environ.get('MASTER_PORT', '0')}"
+    where = os.path.join(tempfile.gettempdir(), name + ".where")
     if comm_rank == 0:
         h = h_or_builder() if callable(h_or_builder) else h_or_builder
+        need = 2 * sum(lv.A.nnz * 16 + (lv.P.nnz * 32 if lv.P is not None else 0) for lv in h.levels)
+        base = os.environ.get("AMGP_SHM")
+        if base is None:  # /dev/shm when it has room (containers often cap it at 64 MB)
+            base = tempfile.gettempdir()
+            if os.path.isdir("/dev/shm") and shutil.disk_usage("/dev/shm").free > need:
+                base = "/dev/shm"
+        path = os.path.join(base, name)
+        shutil.rmtree(path, ignore_errors=True)
+        os.makedirs(path)
         arrs = {"nlev": np.array([len(h.levels)]), "coarse_sweeps": np.array([h.coarse_sweeps])}
         for l, lv in enumerate(h.levels):
             for key, M in (("A", lv.A), ("P", lv.P), ("R", lv.restrict_op() if lv.P is not None else None)):
@@ -232,10 +261,21 @@ def share_hierarchy(h_or_builder, comm_rank, barrier):
                 arrs[f"{key}{l}_shape"] = np.array([M.nrows, M.ncols])
                 arrs[f"{key}{l}_rp"], arrs[f"{key}{l}_ci"], arrs[f"{key}{l}_v"] = M.row_ptr, M.col_idx, M.values
             arrs[f"M{l}"] = np.asarray(lv.M.m_diag)
-        np.savez(path, **arrs)
+        for k, a in arrs.items():
+            np.save(os.path.join(path, k + ".npy"), a)
+        with open(where, "w") as f:
+            f.write(path)
     barrier()
-    d = np.load(path, mmap_mode="r")
-    return d, path
+    if comm_rank != 0:
+        with open(where) as f:
+            path = f.read().strip()
+    return _SharedArrays(path), path
+
+
+def release_shared(path):
+    import shutil
+
+    shutil.rmtree(path, ignore_errors=True)
 
 
 def _mat(d, key):

@@ -116,7 +116,7 @@ def main():
     dist.barrier()
     if me == 0:
         try:
-            os.unlink(path)
+            D.release_shared(path)
         except OSError:
             pass
     dist.destroy_process_group()

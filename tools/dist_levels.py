@@ -92,7 +92,7 @@ def main():
     if comm.rank == 0:
         for r in rows:
             print(json.dumps(r), flush=True)
-        os.unlink(path)
+        D.release_shared(path)
     dist.barrier()
     dist.destroy_process_group()
 

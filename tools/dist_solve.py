@@ -63,7 +63,7 @@ def main():
     if comm.rank == 0:
         print(json.dumps({"grid": args.grid, "world": comm.size, "setup_s": setup, "runs": res}),
               flush=True)
-        os.unlink(path)
+        D.release_shared(path)
     dist.barrier()
     dist.destroy_process_group()
 

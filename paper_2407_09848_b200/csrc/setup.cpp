@@ -489,22 +489,34 @@ int amgp_setup_smooth_prolongator(int64_t n, const int64_t *rp, const int64_t *c
                                   double omega, amgp_hcsr **out) {
     if (n < 0 || !rp || !agg || !out) return amgp_fail(AMGP_EINVAL, "smooth_prolongator: bad argument");
     Cmp A = from_host(n, n, rp, ci, v);
-    // diags(omega/d).tocsr(): one entry per row, zero entries dropped
-    Cmp D;
-    D.nmajor = n;
-    D.nminor = n;
-    D.p.assign(n + 1, 0);
+    // diags(omega/d).tocsr() has one entry per row (zeros dropped); in
+    // csr_matmat(D, A) each output entry gets exactly one contribution
+    // 0.0 + s*a_rk, and the head-inserted linked list emits each row of A
+    // reversed -- built directly.  S's row order matters: it is the summation
+    // order of T = S @ P_hat below.
+    std::vector<double> scale(n);
     for (int64_t r = 0; r < n; r++) {
         const double d = diag_of(A, r);
         if (d == 0.0) return amgp_fail(AMGP_EINVAL, "zero diagonal entry");
-        const double s = omega / d;
-        if (s != 0) {
-            D.i.push_back(r);
-            D.x.push_back(s);
-        }
-        D.p[r + 1] = (int64_t)D.i.size();
+        scale[r] = omega / d;
     }
-    Cmp S = matmat(D, A);
+    Cmp S = build_rows<int>(
+        n, n, [] { return 0; },
+        [&](int64_t r, int &, std::vector<int64_t> &oi, std::vector<double> &ox) {
+            const double s = scale[r];
+            int64_t c = 0;
+            if (s == 0) return c;
+            for (int64_t jj = A.p[r + 1] - 1; jj >= A.p[r]; jj--) {
+                const double prod = s * A.x[jj];
+                const double sum = 0.0 + prod;
+                if (sum != 0) {
+                    oi.push_back(A.i[jj]);
+                    ox.push_back(sum);
+                    c++;
+                }
+            }
+            return c;
+        });
     Cmp Ph = prolongator(n, agg, n_agg);
     Cmp T = matmat(S, Ph);
     Cmp R = binop(Ph, T, [](double a, double b) { return a - b; });

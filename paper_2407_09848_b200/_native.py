@@ -76,6 +76,7 @@ _SIGS = {
     "amgp_mat_to_csr": (C.c_int, [_VP, _P64, _P64, _PD]),
     "amgp_mat_l1_diag": (C.c_int, [_VP, _VP]),
     "amgp_spmv": (C.c_int, [_VP, _VP, _VP, _VP]),
+    "amgp_spmv_timed": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int, C.c_int, _PD]),
     "amgp_fused_update": (C.c_int, [_VP, C.c_int64, C.c_double, C.c_double, C.c_double,
                                      _VP, _VP, _VP, _VP]),
     "amgp_smoother_apply": (C.c_int, [_VP, _VP, _VP, C.POINTER(SmootherCfg), _VP, _VP, _VP]),

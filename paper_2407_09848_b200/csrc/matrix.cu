@@ -404,6 +404,49 @@ int prolong_add_enqueue(amgp_ctx *ctx, const amgp_mat *P, const double *xc, doub
     return launch_rows(ctx, P, xc, SpmvEpi<2>{nullptr, x});
 }
 
+// Diagnostics: reps back-to-back SpMVs (halo exchanges included for a
+// distributed matrix), captured once into a CUDA graph when use_graph, timed
+// with CUDA events on the context stream.  *ms = milliseconds per SpMV.
+extern "C" int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y,
+                               int reps, int use_graph, double *ms) {
+    if (!ctx || !A || reps < 1 || !ms) return amgp_fail(AMGP_EINVAL, "amgp_spmv_timed: bad argument");
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    cudaEvent_t e0, e1;
+    AMGP_CUDA(cudaEventCreate(&e0));
+    AMGP_CUDA(cudaEventCreate(&e1));
+    cudaGraphExec_t exec = nullptr;
+    if (use_graph) {
+        cudaGraph_t g = nullptr;
+        AMGP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        int st = AMGP_OK;
+        for (int i = 0; i < reps && st == AMGP_OK; i++) st = spmv_enqueue(ctx, A, x, y);
+        cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
+        if (st != AMGP_OK) return st;
+        if (e != cudaSuccess) return amgp_cuda_fail(e, "capture", __FILE__, __LINE__);
+        AMGP_CUDA(cudaGraphInstantiate(&exec, g, 0));
+        cudaGraphDestroy(g);
+        AMGP_CUDA(cudaGraphLaunch(exec, ctx->stream));  // warm-up
+    } else {
+        AMGP_TRY(spmv_enqueue(ctx, A, x, y));
+    }
+    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    AMGP_CUDA(cudaEventRecord(e0, ctx->stream));
+    if (use_graph) {
+        AMGP_CUDA(cudaGraphLaunch(exec, ctx->stream));
+    } else {
+        for (int i = 0; i < reps; i++) AMGP_TRY(spmv_enqueue(ctx, A, x, y));
+    }
+    AMGP_CUDA(cudaEventRecord(e1, ctx->stream));
+    AMGP_CUDA(cudaEventSynchronize(e1));
+    float t = 0.f;
+    AMGP_CUDA(cudaEventElapsedTime(&t, e0, e1));
+    *ms = t / reps;
+    if (exec) cudaGraphExecDestroy(exec);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return AMGP_OK;
+}
+
 extern "C" int amgp_spmv(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y) {
     if (!ctx || !A || (!x && A->ncols) || (!y && A->nrows))
         return amgp_fail(AMGP_EINVAL, "amgp_spmv: bad argument");

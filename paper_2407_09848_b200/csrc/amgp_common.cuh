@@ -67,7 +67,15 @@ struct amgp_ctx {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
     double *gather_buf = nullptr;  // allgather scratch for global dots
+    // direct NVLink transport (AMGP_HALO=p2p): peers' halo buffers and flag
+    // words mapped through CUDA IPC; stream memory operations order them
+    int halo_p2p = 0;
+    uint32_t *flags = nullptr;         // [AMGP_MAX_SLOTS][nranks][2] ready / consumed
+    std::vector<uint32_t *> peer_flags;  // every rank's flag array (self included)
+    int next_slot = 0;
 };
+
+#define AMGP_MAX_SLOTS 256
 
 // Halo plan of a row-distributed matrix (dist.cu).  Columns [0, nown) are
 // the rank's own entries of the operand vector; columns >= nown index the
@@ -87,6 +95,11 @@ struct HaloPlan {
     // run, boundary = the two block ends) kernels index slices directly
     // instead of through the list
     std::vector<std::pair<int64_t, int64_t>> interior_runs, boundary_runs;
+    // p2p transport: flag slot, per-peer remote destinations of my data
+    int slot = -1;
+    double **d_dest = nullptr;       // device [npeers] remote base for my segment
+    int64_t *d_seg = nullptr;        // device [npeers + 1] send offsets
+    std::vector<void *> opened;      // IPC-opened peer halo allocations
 };
 
 struct amgp_mat {
@@ -129,6 +142,7 @@ inline SellView view_of(const amgp_mat *A) {
 // it, kernels may gather x through view.xh (dist.cu).
 int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x);
 int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A);
+int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A);  // after the boundary rows
 void mat_free_halo(amgp_mat *A);
 int refresh_slice_maxcol(amgp_mat *A);  // recompute A->slice_maxcol from the device columns
 

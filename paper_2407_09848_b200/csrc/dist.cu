@@ -10,15 +10,49 @@
 // [nown, nown + nhalo) = the halo buffer, filled by one grouped
 // ncclSend/ncclRecv per SpMV.  Row arithmetic does not change with the
 // partition, so every kernel returns the single-GPU bits.
+#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include <algorithm>
 #include <vector>
 
 #include "amgp_common.cuh"
+
+// ---------------------------------------------------------------- direct NVLink transport
+// AMGP_HALO=p2p: instead of NCCL send/recv, the pack kernel stores each
+// neighbour's halo entries straight into the neighbour's halo buffer (CUDA
+// IPC mapping, NVLink stores), and stream memory operations hand over
+// ownership: the sender waits until the receiver has consumed the previous
+// exchange, writes, then sets the receiver's "ready" word; the receiver's
+// stream waits on "ready" before its boundary rows and sets the sender's
+// "consumed" word after them.  No communication kernel, no proxy thread;
+// the waits are done by the stream front end (no spinning kernels).
+typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
+static PFN_streamValue32 g_wait32 = nullptr, g_write32 = nullptr;
+
+static int load_stream_memops() {
+    if (g_wait32 && g_write32) return AMGP_OK;
+    cudaDriverEntryPointQueryResult q1, q2;
+    AMGP_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", (void **)&g_wait32, cudaEnableDefault, &q1));
+    AMGP_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", (void **)&g_write32, cudaEnableDefault, &q2));
+    if (!g_wait32 || !g_write32 || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess)
+        return amgp_fail(AMGP_ECUDA, "stream memory operations unavailable");
+    return AMGP_OK;
+}
+
+#define CU_TRY(call)                                                                      \
+    do {                                                                                  \
+        CUresult _r = (call);                                                             \
+        if (_r != CUDA_SUCCESS) return amgp_fail(AMGP_ECUDA, "driver call failed: " #call); \
+    } while (0)
+
+static inline CUdeviceptr flag_addr(uint32_t *base, int slot, int nranks, int peer, int which) {
+    return (CUdeviceptr)(base + ((size_t)slot * nranks + peer) * 2 + which);
+}
 
 struct NcclApi {
     bool ok = false;
@@ -78,6 +112,53 @@ extern "C" int amgp_comm_unique_id(char *out) {
     return AMGP_OK;
 }
 
+// all-gather `bytes` host bytes per rank through NCCL (setup-time collective)
+static int allgather_host(amgp_ctx *ctx, const void *mine, size_t bytes, std::vector<char> &all) {
+    NcclApi *api = nccl();
+    char *d = nullptr;
+    AMGP_CUDA(cudaMalloc(&d, bytes * (ctx->nranks + 1)));
+    AMGP_CUDA(cudaMemcpy(d + bytes * ctx->nranks, mine, bytes, cudaMemcpyHostToDevice));
+    ncclResult_t r = api->AllGather(d + bytes * ctx->nranks, d, bytes, ncclChar,
+                                    (ncclComm_t)ctx->comm, ctx->stream);
+    if (r != ncclSuccess) {
+        cudaFree(d);
+        return amgp_fail(AMGP_ENCCL, "allgather failed");
+    }
+    all.resize(bytes * ctx->nranks);
+    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    AMGP_CUDA(cudaMemcpy(all.data(), d, all.size(), cudaMemcpyDeviceToHost));
+    cudaFree(d);
+    return AMGP_OK;
+}
+
+static int p2p_init(amgp_ctx *ctx) {
+    AMGP_TRY(load_stream_memops());
+    const int nr = ctx->nranks;
+    const size_t nflags = (size_t)AMGP_MAX_SLOTS * nr * 2;
+    AMGP_CUDA(cudaMalloc(&ctx->flags, nflags * sizeof(uint32_t)));
+    std::vector<uint32_t> init(nflags, 0);
+    for (size_t i = 1; i < nflags; i += 2) init[i] = 1;  // every halo buffer starts consumed
+    AMGP_CUDA(cudaMemcpy(ctx->flags, init.data(), nflags * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    cudaIpcMemHandle_t mine;
+    AMGP_CUDA(cudaIpcGetMemHandle(&mine, ctx->flags));
+    std::vector<char> all;
+    AMGP_TRY(allgather_host(ctx, &mine, sizeof(mine), all));
+    ctx->peer_flags.assign(nr, nullptr);
+    for (int r = 0; r < nr; r++) {
+        if (r == ctx->rank) {
+            ctx->peer_flags[r] = ctx->flags;
+            continue;
+        }
+        cudaIpcMemHandle_t h;
+        memcpy(&h, all.data() + r * sizeof(h), sizeof(h));
+        void *p = nullptr;
+        AMGP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
+        ctx->peer_flags[r] = (uint32_t *)p;
+    }
+    ctx->halo_p2p = 1;
+    return AMGP_OK;
+}
+
 extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const char *id) {
     if (!ctx || !id || nranks < 1 || rank < 0 || rank >= nranks)
         return amgp_fail(AMGP_EINVAL, "amgp_ctx_init_comm: bad argument");
@@ -100,6 +181,11 @@ extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const cha
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_exchanged, cudaEventDisableTiming));
     AMGP_CUDA(cudaMalloc(&ctx->gather_buf, (size_t)nranks * 16 * sizeof(double)));
+    const char *mode = getenv("AMGP_HALO");
+    if (mode && strcmp(mode, "p2p") == 0 && nranks > 1) {
+        if (nranks > 64) return amgp_fail(AMGP_EINVAL, "p2p halo transport supports <= 64 ranks");
+        AMGP_TRY(p2p_init(ctx));
+    }
     return AMGP_OK;
 }
 
@@ -113,6 +199,9 @@ extern "C" int amgp_ctx_comm_info(amgp_ctx *ctx, int *nranks, int *rank) {
 // ---------------------------------------------------------------- halo plans
 static void halo_free(HaloPlan *h) {
     if (!h) return;
+    for (void *p : h->opened) cudaIpcCloseMemHandle(p);
+    cudaFree(h->d_dest);
+    cudaFree(h->d_seg);
     cudaFree(h->send_idx);
     cudaFree(h->sendbuf);
     cudaFree(h->halo);
@@ -124,6 +213,47 @@ static void halo_free(HaloPlan *h) {
 void mat_free_halo(amgp_mat *A) {
     halo_free(A->halo);
     A->halo = nullptr;
+}
+
+// Map where this rank's data lands in each receiver's halo buffer.
+static int p2p_attach(amgp_ctx *ctx, HaloPlan *h) {
+    if (ctx->next_slot >= AMGP_MAX_SLOTS) return amgp_fail(AMGP_EINVAL, "too many distributed matrices");
+    h->slot = ctx->next_slot++;
+    struct Info {
+        cudaIpcMemHandle_t handle;
+        int64_t recv_off[64];
+        int64_t recv_cnt[64];
+    };
+    Info mine;
+    memset(&mine, 0, sizeof(mine));
+    AMGP_CUDA(cudaIpcGetMemHandle(&mine.handle, h->halo));
+    for (size_t q = 0; q < h->peers.size(); q++) {
+        mine.recv_off[h->peers[q]] = h->recv_off[q];
+        mine.recv_cnt[h->peers[q]] = h->recv_cnt[q];
+    }
+    std::vector<char> all;
+    AMGP_TRY(allgather_host(ctx, &mine, sizeof(Info), all));
+    const size_t np = h->peers.size();
+    std::vector<double *> dest(np, nullptr);
+    std::vector<int64_t> seg(np + 1, 0);
+    for (size_t q = 0; q < np; q++) {
+        seg[q] = h->send_off[q];
+        if (h->send_cnt[q] == 0) continue;
+        Info peer;
+        memcpy(&peer, all.data() + h->peers[q] * sizeof(Info), sizeof(Info));
+        if (peer.recv_cnt[ctx->rank] != h->send_cnt[q])
+            return amgp_fail(AMGP_EINVAL, "halo plans of neighbouring ranks disagree");
+        void *base = nullptr;
+        AMGP_CUDA(cudaIpcOpenMemHandle(&base, peer.handle, cudaIpcMemLazyEnablePeerAccess));
+        h->opened.push_back(base);
+        dest[q] = (double *)base + peer.recv_off[ctx->rank];
+    }
+    seg[np] = h->nsend;
+    AMGP_CUDA(cudaMalloc(&h->d_dest, std::max<size_t>(np, 1) * sizeof(double *)));
+    AMGP_CUDA(cudaMalloc(&h->d_seg, (np + 1) * sizeof(int64_t)));
+    if (np) AMGP_CUDA(cudaMemcpy(h->d_dest, dest.data(), np * sizeof(double *), cudaMemcpyHostToDevice));
+    AMGP_CUDA(cudaMemcpy(h->d_seg, seg.data(), (np + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    return AMGP_OK;
 }
 
 extern "C" int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const int *peers,
@@ -191,6 +321,13 @@ extern "C" int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const in
         halo_free(h);
         return amgp_cuda_fail(e, "halo plan upload", __FILE__, __LINE__);
     }
+    if (ctx->halo_p2p) {  // collective: every rank attaches its plans in the same order
+        int st = p2p_attach(ctx, h);
+        if (st != AMGP_OK) {
+            halo_free(h);
+            return st;
+        }
+    }
     mat_free_halo(A);
     A->halo = h;
     return AMGP_OK;
@@ -214,8 +351,67 @@ __global__ void k_pack(int64_t n, const int64_t *__restrict__ idx, const double 
         out[i] = x[idx[i]];
 }
 
+// p2p pack: entry i of the send list goes straight to its receiver's halo
+__global__ void k_pack_p2p(int64_t n, int npeers, const int64_t *__restrict__ idx,
+                           const double *__restrict__ x, double *const *__restrict__ dest,
+                           const int64_t *__restrict__ seg) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int q = 0;
+        while (q + 1 < npeers && i >= seg[q + 1]) q++;
+        dest[q][i - seg[q]] = x[idx[i]];
+    }
+}
+
+static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
+    CUstream s = (CUstream)ctx->stream;
+    const int nr = ctx->nranks, me = ctx->rank;
+    for (size_t q = 0; q < h.peers.size(); q++) {  // receiver done with the previous data
+        if (h.send_cnt[q] == 0) continue;
+        const CUdeviceptr consumed = flag_addr(ctx->flags, h.slot, nr, h.peers[q], 1);
+        CU_TRY(g_wait32(s, consumed, 1, CU_STREAM_WAIT_VALUE_EQ));
+        CU_TRY(g_write32(s, consumed, 0, CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER));
+    }
+    if (h.nsend > 0) {
+        const unsigned g = (unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 8);
+        k_pack_p2p<<<g, 256, 0, ctx->stream>>>(h.nsend, (int)h.peers.size(), h.send_idx, x, h.d_dest,
+                                              h.d_seg);
+        AMGP_CHECK_LAUNCH(ctx);
+    }
+    for (size_t q = 0; q < h.peers.size(); q++) {  // data in place: signal (after a memory fence)
+        if (h.send_cnt[q] == 0) continue;
+        CU_TRY(g_write32(s, flag_addr(ctx->peer_flags[h.peers[q]], h.slot, nr, me, 0), 1,
+                         CU_STREAM_WRITE_VALUE_DEFAULT));
+    }
+    return AMGP_OK;
+}
+
+static int p2p_end(amgp_ctx *ctx, const HaloPlan &h) {
+    CUstream s = (CUstream)ctx->stream;
+    for (size_t q = 0; q < h.peers.size(); q++) {
+        if (h.recv_cnt[q] == 0) continue;
+        const CUdeviceptr ready = flag_addr(ctx->flags, h.slot, ctx->nranks, h.peers[q], 0);
+        CU_TRY(g_wait32(s, ready, 1, CU_STREAM_WAIT_VALUE_EQ));
+        CU_TRY(g_write32(s, ready, 0, CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER));
+    }
+    return AMGP_OK;
+}
+
+int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A) {
+    if (!ctx->halo_p2p) return AMGP_OK;
+    const HaloPlan &h = *A->halo;
+    CUstream s = (CUstream)ctx->stream;
+    for (size_t q = 0; q < h.peers.size(); q++) {  // boundary rows read the halo: release it
+        if (h.recv_cnt[q] == 0) continue;
+        CU_TRY(g_write32(s, flag_addr(ctx->peer_flags[h.peers[q]], h.slot, ctx->nranks, ctx->rank, 1),
+                         1, CU_STREAM_WRITE_VALUE_DEFAULT));
+    }
+    return AMGP_OK;
+}
+
 int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
     const HaloPlan &h = *A->halo;
+    if (ctx->halo_p2p) return p2p_begin(ctx, h, x);
     NcclApi *api = nccl();
     if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator for the halo exchange");
     if (h.nsend > 0) {
@@ -241,7 +437,7 @@ int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
 }
 
 int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A) {
-    (void)A;
+    if (ctx->halo_p2p) return p2p_end(ctx, *A->halo);
     AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
     return AMGP_OK;
 }

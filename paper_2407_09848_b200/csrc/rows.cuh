@@ -135,5 +135,6 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     };
     AMGP_TRY(launch_set(h.interior_runs, h.interior, h.n_interior));
     AMGP_TRY(halo_exchange_end(ctx, A));
-    return launch_set(h.boundary_runs, h.boundary, h.n_boundary);
+    AMGP_TRY(launch_set(h.boundary_runs, h.boundary, h.n_boundary));
+    return halo_exchange_done(ctx, A);
 }

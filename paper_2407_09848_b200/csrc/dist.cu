@@ -47,7 +47,8 @@ static int load_stream_memops() {
 #define CU_TRY(call)                                                                      \
     do {                                                                                  \
         CUresult _r = (call);                                                             \
-        if (_r != CUDA_SUCCESS) return amgp_fail(AMGP_ECUDA, "driver call failed: " #call); \
+        if (_r != CUDA_SUCCESS)                                                           \
+            return amgp_fail(AMGP_ECUDA, "driver call failed (CUresult " + std::to_string((int)_r) + "): " #call); \
     } while (0)
 
 static inline CUdeviceptr flag_addr(uint32_t *base, int slot, int nranks, int peer, int which) {
@@ -370,7 +371,7 @@ static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
         if (h.send_cnt[q] == 0) continue;
         const CUdeviceptr consumed = flag_addr(ctx->flags, h.slot, nr, h.peers[q], 1);
         CU_TRY(g_wait32(s, consumed, 1, CU_STREAM_WAIT_VALUE_EQ));
-        CU_TRY(g_write32(s, consumed, 0, CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER));
+        CU_TRY(g_write32(s, consumed, 0, CU_STREAM_WRITE_VALUE_DEFAULT));
     }
     if (h.nsend > 0) {
         const unsigned g = (unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 8);
@@ -392,7 +393,7 @@ static int p2p_end(amgp_ctx *ctx, const HaloPlan &h) {
         if (h.recv_cnt[q] == 0) continue;
         const CUdeviceptr ready = flag_addr(ctx->flags, h.slot, ctx->nranks, h.peers[q], 0);
         CU_TRY(g_wait32(s, ready, 1, CU_STREAM_WAIT_VALUE_EQ));
-        CU_TRY(g_write32(s, ready, 0, CU_STREAM_WRITE_VALUE_NO_MEMORY_BARRIER));
+        CU_TRY(g_write32(s, ready, 0, CU_STREAM_WRITE_VALUE_DEFAULT));
     }
     return AMGP_OK;
 }

@@ -24,7 +24,12 @@
 #define ROWS_BLOCK 256
 #define ROWS_SLICES (ROWS_BLOCK / 32)
 #define ROWS_U 8
-#define SPLIT_WARPS 16
+#ifndef SPLIT_WARPS
+#define SPLIT_WARPS 32
+#endif
+#ifndef SPLIT_U
+#define SPLIT_U 8  // slot loads in flight per thread
+#endif
 #define SPLIT_CHUNK 192  // slots staged per pass: 192 * 32 * 8 B = 48 KB
 
 template <class Epi>
@@ -52,11 +57,11 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     double sum = 0.0;
     for (int j0 = 0; j0 < w; j0 += SPLIT_CHUNK) {
         const int jn = min(SPLIT_CHUNK, w - j0);
-        for (int j = warp; j < jn; j += SPLIT_WARPS * 4) {
-            int32_t cc[4];
-            double vv[4];
+        for (int j = warp; j < jn; j += SPLIT_WARPS * SPLIT_U) {
+            int32_t cc[SPLIT_U];
+            double vv[SPLIT_U];
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < SPLIT_U; u++) {
                 const int jj = j + u * SPLIT_WARPS;
                 const bool ok = jj < jn;
                 const int64_t o = base + (int64_t)(j0 + jj) * 32 + lane;
@@ -64,7 +69,7 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                 vv[u] = ok ? ld_stream_f64(A.val + o, pf) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < 4; u++) {
+            for (int u = 0; u < SPLIT_U; u++) {
                 const int jj = j + u * SPLIT_WARPS;
                 if (jj < jn) {
                     double p = 0.0;
@@ -76,8 +81,10 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
             }
         }
         __syncthreads();
-        if (warp == 0)
+        if (warp == 0) {
+#pragma unroll 8
             for (int j = 0; j < jn; j++) sum = __dadd_rn(sum, prod[j * 32 + lane]);
+        }
         __syncthreads();
     }
     if (warp == 0) {

@@ -47,17 +47,21 @@ def up_to_date():
     return all(os.path.getmtime(p) <= t for p in sources() + headers())
 
 
-def build(force=False, verbose=False):
-    if not force and up_to_date():
+def build(force=False, verbose=False, defines=(), lib=None):
+    """Compile every csrc/ translation unit and link libamgp.so.  `defines`
+    (e.g. ["SPLIT_WARPS=16"]) and `lib` build a tuning variant elsewhere."""
+    target = lib or LIB
+    if not force and not defines and lib is None and up_to_date():
         return LIB
     objs = []
-    odir = os.path.join(PKG, "build")
+    odir = os.path.join(PKG, "build", "variant_" + "_".join(d.replace("=", "") for d in defines)
+                        if defines else "")
     os.makedirs(odir, exist_ok=True)
     procs = []
     for src in sources():
         obj = os.path.join(odir, os.path.splitext(os.path.basename(src))[0] + ".o")
-        cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "--shared"], "-c",
-               src, "-o", obj]
+        cmd = [NVCC, *ARCH, *[f for f in FLAGS if f != "--shared"], *[f"-D{d}" for d in defines],
+               "-c", src, "-o", obj]
         if verbose:
             print(" ".join(cmd))
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
@@ -73,13 +77,15 @@ def build(force=False, verbose=False):
     if failed:
         msg = "\n".join(f"--- {s}\n{t}" for s, t in failed)
         raise RuntimeError(f"nvcc failed:\n{msg}")
-    cmd = [NVCC, *ARCH, "--shared", "-o", LIB, *objs, *LIBS]
+    cmd = [NVCC, *ARCH, "--shared", "-o", target, *objs, *LIBS]
     if verbose:
         print(" ".join(cmd))
     subprocess.run(cmd, check=True)
-    return LIB
+    return target
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose=True)
-    print("built", LIB)
+    # python -m paper_2407_09848_b200._build [--force] [-DNAME=VAL ... -o variant.so]
+    defs = [a[2:] for a in sys.argv[1:] if a.startswith("-D")]
+    out = sys.argv[sys.argv.index("-o") + 1] if "-o" in sys.argv else None
+    print("built", build(force="--force" in sys.argv, verbose=True, defines=defs, lib=out))

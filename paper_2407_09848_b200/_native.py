@@ -19,7 +19,7 @@ import threading
 import numpy as np
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libamgp.so")
+LIB_PATH = os.environ.get("AMGP_LIB", os.path.join(PKG, "libamgp.so"))  # override: tuning variants
 
 AMGP_OK = 0
 AMGP_EINVAL = -1

@@ -25,10 +25,10 @@
 #define ROWS_SLICES (ROWS_BLOCK / 32)
 #define ROWS_U 8
 #ifndef SPLIT_WARPS
-#define SPLIT_WARPS 32
+#define SPLIT_WARPS 16  // measured best of {8,16,32} x {4,8} (tools: AMGP_LIB variants)
 #endif
 #ifndef SPLIT_U
-#define SPLIT_U 8  // slot loads in flight per thread
+#define SPLIT_U 4  // slot loads in flight per thread
 #endif
 #define SPLIT_CHUNK 192  // slots staged per pass: 192 * 32 * 8 B = 48 KB
 

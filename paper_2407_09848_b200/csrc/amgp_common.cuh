@@ -212,8 +212,10 @@ __device__ __forceinline__ double ld_gather_f64(const double *p, uint64_t pol) {
 // Row sum of slice row `lane` of slice `s`: sum_j val*x[col] from 0.0 in slot
 // order (== CSR stored order).  Slots are loaded U at a time (predicated) so
 // a warp keeps 2U streaming loads + U gathers in flight.  Padding slots
-// (col < 0) contribute nothing.
-template <int U>
+// (col < 0) contribute nothing.  HALO: columns >= A.nown read the halo
+// buffer A.xh (boundary slices of a distributed matrix); every other launch
+// takes the plain single-load gather.
+template <int U, bool HALO = false>
 __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int lane,
                                                const double *__restrict__ x) {
     const int64_t base = A.slice_ptr[s];
@@ -232,10 +234,13 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
             vv[u] = ok ? ld_stream_f64(v + (int64_t)(j + u) * AMGP_SLICE, pf) : 0.0;
         }
 #pragma unroll
-        for (int u = 0; u < U; u++)
-            xx[u] = cc[u] < 0 ? 0.0
-                              : (cc[u] < A.nown ? ld_gather_f64(x + cc[u], pl)
-                                                : ld_gather_f64(A.xh + (cc[u] - A.nown), pl));
+        for (int u = 0; u < U; u++) {
+            if (HALO)
+                xx[u] = cc[u] < 0 ? 0.0
+                                  : ld_gather_f64(cc[u] < A.nown ? x + cc[u] : A.xh + (cc[u] - A.nown), pl);
+            else
+                xx[u] = cc[u] < 0 ? 0.0 : ld_gather_f64(x + cc[u], pl);
+        }
 #pragma unroll
         for (int u = 0; u < U; u++)
             if (cc[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(vv[u], xx[u]));

@@ -5,6 +5,11 @@
 
 #include "rows.cuh"
 
+// m, b and the gathered operand are never written by the kernel that reads
+// them (the operand already travels through the non-coherent path in
+// sell_row_dot), so their row loads take it too.
+__device__ __forceinline__ double ro(const double *p, int64_t i) { return __ldg(p + i); }
+
 // ---------------------------------------------------------------- epilogues
 template <bool FIRST, bool LAST, bool X0>
 struct Cheb4Step {
@@ -17,10 +22,10 @@ struct Cheb4Step {
     double *x;
     double cz, cr, beta;
     __device__ __forceinline__ void operator()(int64_t row, double y) const {
-        const double rr = __dsub_rn(FIRST ? b[row] : r[row], y);
-        double z = FIRST ? __dmul_rn(0.0, cz) : __dmul_rn(xg[row], cz);
-        z = __dadd_rn(z, __dmul_rn(cr, __ddiv_rn(rr, m[row])));
-        const double xo = FIRST ? (X0 ? xg[row] : 0.0) : x[row];
+        const double rr = __dsub_rn(FIRST ? ro(b, row) : r[row], y);
+        double z = FIRST ? __dmul_rn(0.0, cz) : __dmul_rn(ro(xg, row), cz);
+        z = __dadd_rn(z, __dmul_rn(cr, __ddiv_rn(rr, ro(m, row))));
+        const double xo = FIRST ? (X0 ? ro(xg, row) : 0.0) : x[row];
         x[row] = __dadd_rn(xo, __dmul_rn(beta, z));
         if (!LAST) {
             r[row] = rr;
@@ -42,15 +47,15 @@ struct Cheb1Step {
     __device__ __forceinline__ void operator()(int64_t row, double y) const {
         double rr, d, xo;
         if (FIRST) {
-            rr = __ddiv_rn(__dsub_rn(b[row], y), m[row]);
+            rr = __ddiv_rn(__dsub_rn(ro(b, row), y), ro(m, row));
             if (!RHO1) rr = __ddiv_rn(rr, rho);
             d = __ddiv_rn(rr, c0);
-            xo = X0 ? xg[row] : 0.0;
+            xo = X0 ? ro(xg, row) : 0.0;
         } else {
-            double sv = __ddiv_rn(y, m[row]);
+            double sv = __ddiv_rn(y, ro(m, row));
             if (!RHO1) sv = __ddiv_rn(sv, rho);
             rr = __dsub_rn(r[row], sv);
-            d = __dadd_rn(__dmul_rn(xg[row], c0), __dmul_rn(c1, rr));
+            d = __dadd_rn(__dmul_rn(ro(xg, row), c0), __dmul_rn(c1, rr));
             xo = x[row];
         }
         x[row] = __dadd_rn(xo, d);
@@ -69,8 +74,8 @@ struct L1Sweep {
     const double *xin;
     double *xout;
     __device__ __forceinline__ void operator()(int64_t row, double y) const {
-        const double rr = __dsub_rn(b[row], y);
-        xout[row] = __dadd_rn(X0 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
+        const double rr = __dsub_rn(ro(b, row), y);
+        xout[row] = __dadd_rn(X0 ? ro(xin, row) : 0.0, __ddiv_rn(rr, ro(m, row)));
     }
 };
 

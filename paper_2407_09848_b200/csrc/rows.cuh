@@ -32,24 +32,28 @@
 #endif
 #define SPLIT_CHUNK 192  // slots staged per pass: 192 * 32 * 8 B = 48 KB
 
-template <class Epi>
+// GEN = false: slices s0 .. s0+nlist-1, every column local (single-GPU
+// matrices, interior slices of distributed ones).  GEN = true: a slice list
+// and/or halo columns (boundary slices) -- kept out of the common kernel so
+// its gather stays one load per slot.
+template <class Epi, bool GEN>
 __global__ void __launch_bounds__(ROWS_BLOCK)
 k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     const int64_t idx = (int64_t)blockIdx.x * ROWS_SLICES + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
     if (idx >= A.nlist) return;
-    const int64_t s = A.slist ? (int64_t)A.slist[idx] : A.s0 + idx;
+    const int64_t s = GEN && A.slist ? (int64_t)A.slist[idx] : A.s0 + idx;
     double y = 0.0;
-    if (Epi::kSpmv) y = sell_row_dot<ROWS_U>(A, s, lane, xg);
+    if (Epi::kSpmv) y = sell_row_dot<ROWS_U, GEN>(A, s, lane, xg);
     const int64_t row = s * 32 + lane;
     if (row < A.nrows) epi(row, y);
 }
 
-template <class Epi>
+template <class Epi, bool GEN>
 __global__ void __launch_bounds__(SPLIT_WARPS * 32)
 k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     __shared__ double prod[SPLIT_CHUNK * 32];
-    const int64_t s = A.slist ? (int64_t)A.slist[blockIdx.x] : A.s0 + (int64_t)blockIdx.x;
+    const int64_t s = GEN && A.slist ? (int64_t)A.slist[blockIdx.x] : A.s0 + (int64_t)blockIdx.x;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
@@ -74,8 +78,8 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                 if (jj < jn) {
                     double p = 0.0;
                     if (cc[u] >= 0)
-                        p = __dmul_rn(vv[u], cc[u] < A.nown ? ld_gather_f64(xg + cc[u], pl)
-                                                            : ld_gather_f64(A.xh + (cc[u] - A.nown), pl));
+                        p = __dmul_rn(vv[u], ld_gather_f64(GEN && cc[u] >= A.nown ? A.xh + (cc[u] - A.nown)
+                                                                                   : xg + cc[u], pl));
                     prod[jj * 32 + lane] = p;
                 }
             }
@@ -103,10 +107,15 @@ template <class Epi>
 int launch_view(amgp_ctx *ctx, const amgp_mat *A, const SellView &v, const double *xg,
                 const Epi &epi) {
     if (v.nlist == 0) return AMGP_OK;
-    if (Epi::kSpmv && use_split(A))
-        k_split_rows<Epi><<<(unsigned)v.nlist, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
-    else
-        k_thread_rows<Epi><<<grid_for(v.nlist, ROWS_SLICES), ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
+    const bool gen = v.slist || v.xh;
+    const unsigned gs = (unsigned)v.nlist, gt = grid_for(v.nlist, ROWS_SLICES);
+    if (Epi::kSpmv && use_split(A)) {
+        if (gen) k_split_rows<Epi, true><<<gs, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+        else k_split_rows<Epi, false><<<gs, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+    } else {
+        if (gen) k_thread_rows<Epi, true><<<gt, ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
+        else k_thread_rows<Epi, false><<<gt, ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
+    }
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }
@@ -121,8 +130,6 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     const HaloPlan &h = *A->halo;
     AMGP_TRY(halo_exchange_begin(ctx, A, xg));
     SellView v = view_of(A);
-    v.nown = h.nown;
-    v.xh = h.halo;
     // one launch per run when the set is a few contiguous runs, else the list
     auto launch_set = [&](const std::vector<std::pair<int64_t, int64_t>> &runs,
                           const int32_t *list, int64_t n) -> int {
@@ -140,8 +147,13 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
         v.nlist = n;
         return launch_view(ctx, A, v, xg, epi);
     };
+    // interior slices have no halo column (slice_maxcol < nown): plain gather
+    v.nown = INT64_MAX;
+    v.xh = nullptr;
     AMGP_TRY(launch_set(h.interior_runs, h.interior, h.n_interior));
     AMGP_TRY(halo_exchange_end(ctx, A));
+    v.nown = h.nown;
+    v.xh = h.halo;
     AMGP_TRY(launch_set(h.boundary_runs, h.boundary, h.n_boundary));
     return halo_exchange_done(ctx, A);
 }

@@ -49,8 +49,12 @@ k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     if (row < A.nrows) epi(row, y);
 }
 
-template <class Epi, bool GEN>
-__global__ void __launch_bounds__(SPLIT_WARPS * 32)
+// NW warps, U slot loads in flight per thread: SPLIT_WARPS x SPLIT_U for
+// levels with enough slices to fill the GPU; a launch with fewer slices than
+// two per SM is latency bound (a slice's chunk costs ceil(192 / (NW U))
+// dependent column->gather rounds), so it takes 24 warps x 8 = one round.
+template <class Epi, bool GEN, int NW, int U>
+__global__ void __launch_bounds__(NW * 32)
 k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     __shared__ double prod[SPLIT_CHUNK * 32];
     const int64_t s = GEN && A.slist ? (int64_t)A.slist[blockIdx.x] : A.s0 + (int64_t)blockIdx.x;
@@ -61,20 +65,20 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     double sum = 0.0;
     for (int j0 = 0; j0 < w; j0 += SPLIT_CHUNK) {
         const int jn = min(SPLIT_CHUNK, w - j0);
-        for (int j = warp; j < jn; j += SPLIT_WARPS * SPLIT_U) {
-            int32_t cc[SPLIT_U];
-            double vv[SPLIT_U];
+        for (int j = warp; j < jn; j += NW * U) {
+            int32_t cc[U];
+            double vv[U];
 #pragma unroll
-            for (int u = 0; u < SPLIT_U; u++) {
-                const int jj = j + u * SPLIT_WARPS;
+            for (int u = 0; u < U; u++) {
+                const int jj = j + u * NW;
                 const bool ok = jj < jn;
                 const int64_t o = base + (int64_t)(j0 + jj) * 32 + lane;
                 cc[u] = ok ? ld_stream_s32(A.col + o, pf) : -1;
                 vv[u] = ok ? ld_stream_f64(A.val + o, pf) : 0.0;
             }
 #pragma unroll
-            for (int u = 0; u < SPLIT_U; u++) {
-                const int jj = j + u * SPLIT_WARPS;
+            for (int u = 0; u < U; u++) {
+                const int jj = j + u * NW;
                 if (jj < jn) {
                     double p = 0.0;
                     if (cc[u] >= 0)
@@ -110,8 +114,13 @@ int launch_view(amgp_ctx *ctx, const amgp_mat *A, const SellView &v, const doubl
     const bool gen = v.slist || v.xh;
     const unsigned gs = (unsigned)v.nlist, gt = grid_for(v.nlist, ROWS_SLICES);
     if (Epi::kSpmv && use_split(A)) {
-        if (gen) k_split_rows<Epi, true><<<gs, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
-        else k_split_rows<Epi, false><<<gs, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+        if (v.nlist < 2 * 148) {
+            if (gen) k_split_rows<Epi, true, 24, 8><<<gs, 24 * 32, 0, ctx->stream>>>(v, xg, epi);
+            else k_split_rows<Epi, false, 24, 8><<<gs, 24 * 32, 0, ctx->stream>>>(v, xg, epi);
+        } else {
+            if (gen) k_split_rows<Epi, true, SPLIT_WARPS, SPLIT_U><<<gs, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+            else k_split_rows<Epi, false, SPLIT_WARPS, SPLIT_U><<<gs, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+        }
     } else {
         if (gen) k_thread_rows<Epi, true><<<gt, ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
         else k_thread_rows<Epi, false><<<gt, ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);

@@ -85,17 +85,23 @@ struct amgp_hier {
     std::mutex mu;
 };
 
-#define COARSE_SMEM_BYTES (200 * 1024)
+#define COARSE_SMEM_BYTES (227 * 1024)
+#define TAIL_COARSE_SMEM (200 * 1024)  // K8's coarse phase (products staged)
 
-static inline size_t coarse_smem(const amgp_mat *A) {
-    return 16 * (size_t)A->nrows + 20 * (size_t)A->stored + 64;
+// Shared memory of k_coarse_l1: two iterates + the level's SELL values and
+// columns (+ one product per slot when PROD).
+static inline size_t coarse_smem(const amgp_mat *A, bool prod) {
+    return 16 * (size_t)A->nrows + (prod ? 20 : 12) * (size_t)A->stored + 64;
 }
 
 // K6: all l1-Jacobi sweeps of the coarsest level in one CTA.  The level's
-// SELL slots are staged in shared memory once; per sweep every (row, slot)
-// product is formed in parallel by all threads, then each row is summed in
-// slot order (padding contributes +0.0, bitwise neutral -- rows.cuh) and
-// updated as k_l1_sweep does, so the result is bitwise the multi-launch one.
+// SELL slots are staged in shared memory once.  PROD: per sweep every
+// (row, slot) product is formed in parallel by all threads, then each row is
+// summed in slot order (padding contributes +0.0, bitwise neutral --
+// rows.cuh); without room for the products each row thread forms its own in
+// slot order (same operations, same order).  Rows are updated as
+// k_l1_sweep does, so the result is bitwise the multi-launch one.
+template <bool PROD>
 __global__ void __launch_bounds__(1024)
 k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__ b,
             double *__restrict__ x, int sweeps) {
@@ -105,7 +111,7 @@ k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__
     double *buf[2] = {sh, sh + n};
     double *pv = sh + 2 * n;
     double *prod = pv + stored;
-    int32_t *pc = (int32_t *)(prod + stored);
+    int32_t *pc = (int32_t *)(prod + (PROD ? stored : 0));
     for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
         pv[e] = A.val[e];
         pc[e] = A.col[e];
@@ -114,7 +120,7 @@ k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__
     for (int s = 1; s <= sweeps; s++) {
         const double *xin = buf[(s - 1) & 1];
         double *xout = buf[s & 1];
-        if (s > 1) {
+        if (PROD && s > 1) {
             for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
                 const int32_t c = pc[e];
                 prod[e] = c >= 0 ? __dmul_rn(pv[e], xin[c]) : 0.0;
@@ -128,9 +134,19 @@ k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__
                 const int lane = row & 31;
                 const int64_t base = A.slice_ptr[sl];
                 const int w = (int)((A.slice_ptr[sl + 1] - base) >> 5);
-                const double *pp = prod + base + lane;
+                if (PROD) {
+                    const double *pp = prod + base + lane;
 #pragma unroll 8
-                for (int j = 0; j < w; j++) y = __dadd_rn(y, pp[j * 32]);
+                    for (int j = 0; j < w; j++) y = __dadd_rn(y, pp[j * 32]);
+                } else {
+                    const double *vv = pv + base + lane;
+                    const int32_t *cc = pc + base + lane;
+#pragma unroll 8
+                    for (int j = 0; j < w; j++) {
+                        const int32_t c = cc[j * 32];
+                        if (c >= 0) y = __dadd_rn(y, __dmul_rn(vv[j * 32], xin[c]));
+                    }
+                }
             }
             const double rr = __dsub_rn(b[row], y);
             xout[row] = __dadd_rn(s > 1 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
@@ -185,8 +201,15 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
     }
     if (h->coarse_solver == AMGP_COARSE_SMOOTHER)
         return smoother_enqueue(ctx, A, h->m[l], h->plan[l], r, nullptr, z, h->work[l]);
-    if (!A->halo && coarse_smem(A) <= COARSE_SMEM_BYTES) {
-        k_coarse_l1<<<1, 1024, coarse_smem(A), ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
+    if (!A->halo && coarse_smem(A, true) <= COARSE_SMEM_BYTES) {
+        k_coarse_l1<true><<<1, 1024, coarse_smem(A, true), ctx->stream>>>(view_of(A), h->m[l], r, z,
+                                                                           h->coarse_sweeps);
+        AMGP_CHECK_LAUNCH(ctx);
+        return AMGP_OK;
+    }
+    if (!A->halo && coarse_smem(A, false) <= COARSE_SMEM_BYTES) {
+        k_coarse_l1<false><<<1, 1024, coarse_smem(A, false), ctx->stream>>>(view_of(A), h->m[l], r, z,
+                                                                            h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
@@ -415,7 +438,7 @@ static void tail_plan(amgp_hier *h) {
     if (!h->use_tail || h->coarse_solver != AMGP_COARSE_L1_JACOBI) return;
     const int Lc = h->nlev - 1;
     amgp_mat *C = h->A[Lc];
-    if (C->halo || coarse_smem(C) > COARSE_SMEM_BYTES || C->nrows > TAIL_MAX_ROWS) return;
+    if (C->halo || coarse_smem(C, true) > TAIL_COARSE_SMEM || C->nrows > TAIL_MAX_ROWS) return;
     int start = Lc;
     for (int l = Lc - 1; l >= 0 && Lc - l < TAIL_MAX_LEV; l--) {
         const amgp_mat *A = h->A[l];
@@ -464,7 +487,7 @@ static int tail_prepare(amgp_hier *h) {
     if (!h->d_tail) AMGP_CUDA(cudaMalloc(&h->d_tail, sizeof(TailDesc)));
     AMGP_CUDA(cudaStreamSynchronize(h->ctx->stream));
     AMGP_CUDA(cudaMemcpy(h->d_tail, &d, sizeof(TailDesc), cudaMemcpyHostToDevice));
-    h->tail_smem = std::max<size_t>((size_t)TAIL_CHUNK * 32 * sizeof(double), coarse_smem(h->A[h->nlev - 1]));
+    h->tail_smem = std::max<size_t>((size_t)TAIL_CHUNK * 32 * sizeof(double), coarse_smem(h->A[h->nlev - 1], true));
     AMGP_CUDA(cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)h->tail_smem));
     int per_sm = 0, nsm = 0;
@@ -611,8 +634,10 @@ extern "C" int amgp_hier_create(amgp_ctx *ctx, int nlevels, amgp_mat *const *A,
         delete h;
         return amgp_cuda_fail(e, "hierarchy buffers", __FILE__, __LINE__);
     }
-    // K6 needs up to 96 KB of dynamic shared memory
-    cudaFuncSetAttribute(k_coarse_l1, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    // K6 stages the coarsest level in up to 227 KB of dynamic shared memory
+    cudaFuncSetAttribute(k_coarse_l1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         COARSE_SMEM_BYTES);
+    cudaFuncSetAttribute(k_coarse_l1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          COARSE_SMEM_BYTES);
     cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     *out = h;

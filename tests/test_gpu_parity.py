@@ -484,3 +484,45 @@ def test_single_reduction_pcg_iterations(P, kind):
     x, rep = P.solve(T, np.ones(40), cfg=P.KrylovConfig(tol=1e-10, itmax=200, variant="pcg1"))
     assert rep.converged
     assert np.linalg.norm(np.ones(40) - T.to_dense() @ x) / np.sqrt(40) <= 1e-9
+
+
+@pytest.mark.parametrize("nc", [40, 121])
+def test_coarse_solve_shared_memory_variants_bitwise(P, nc):
+    """Coarsest-level l1 sweeps in one CTA: nc = 40 stages the slot products
+    in shared memory, nc = 121 (dense, 311 KB with products) forms them per
+    row from the staged slots -- both bitwise equal to the oracle V-cycle."""
+    import scipy.sparse as sp
+
+    A0, _ = P.poisson3d(11)
+    n0 = A0.nrows
+    rng = np.random.default_rng(nc)
+    agg = np.minimum(np.arange(n0) * nc // n0, nc - 1)
+    Pm = sp.csr_matrix((rng.uniform(0.5, 1.5, n0), (np.arange(n0), agg)), shape=(n0, nc))
+    B = rng.standard_normal((nc, nc))
+    A1 = sp.csr_matrix(B @ B.T + nc * np.eye(nc))
+
+    def csr(M):
+        M = sp.csr_matrix(M)
+        M.sort_indices()
+        return P.CsrMatrix(M.shape[0], M.shape[1], M.indptr, M.indices, M.data)
+
+    C0, C1, CP, CR = A0, csr(A1), csr(Pm), csr(Pm.T)
+    M0, M1 = P.l1_jacobi_diag(C0), P.l1_jacobi_diag(C1)
+    m0, m1 = np.asarray(M0.m_diag), np.asarray(M1.m_diag)
+    params = smoother_params()
+    r = rng.standard_normal(n0)
+    for fam in FAMILIES:
+        k = 3
+        cfg = P.PolySmootherConfig(family=fam, degree=k)
+        lv0 = P.Level(A=C0, M=M0, smoother=cfg, P=CP)
+        lv0._Pt = CR
+        lv1 = P.Level(A=C1, M=M1, smoother=cfg)
+        h = P.AmgHierarchy(levels=[lv0, lv1])
+        got = P.vcycle_apply(h, r)
+        a = params["a_star"][str(k)] if fam == "opt_cheb1" else 0.0
+        beta = np.array(params["beta"][str(k)]) if fam == "opt_cheb4" else None
+        ol = [{"A": (C0.row_ptr, C0.col_idx, C0.values), "m": m0,
+               "P": (CP.row_ptr, CP.col_idx, CP.values), "R": (CR.row_ptr, CR.col_idx, CR.values)},
+              {"A": (C1.row_ptr, C1.col_idx, C1.values), "m": m1}]
+        want = oracle.Hierarchy(ol, fam, k, a=a, beta=beta).vcycle(r)
+        assert np.array_equal(got, want), fam

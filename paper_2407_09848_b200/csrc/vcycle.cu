@@ -87,21 +87,20 @@ struct amgp_hier {
 
 #define COARSE_SMEM_BYTES (227 * 1024)
 #define TAIL_COARSE_SMEM (200 * 1024)  // K8's coarse phase (products staged)
-
-// Shared memory of k_coarse_l1: two iterates + the level's SELL values and
-// columns (+ one product per slot when PROD).
-static inline size_t coarse_smem(const amgp_mat *A, bool prod) {
-    return 16 * (size_t)A->nrows + (prod ? 20 : 12) * (size_t)A->stored + 64;
+static inline size_t tail_coarse_smem(const amgp_mat *A) {
+    return 16 * (size_t)A->nrows + 20 * (size_t)A->stored + 64;
 }
 
-// K6: all l1-Jacobi sweeps of the coarsest level in one CTA.  The level's
-// SELL slots are staged in shared memory once.  PROD: per sweep every
-// (row, slot) product is formed in parallel by all threads, then each row is
-// summed in slot order (padding contributes +0.0, bitwise neutral --
-// rows.cuh); without room for the products each row thread forms its own in
-// slot order (same operations, same order).  Rows are updated as
-// k_l1_sweep does, so the result is bitwise the multi-launch one.
-template <bool PROD>
+// K6 for coarsest levels too large for k_coarse_l1_reg (below): all
+// l1-Jacobi sweeps in one CTA with the level's SELL values and columns staged
+// in shared memory; each row thread forms its products and sums them in slot
+// order (padding skipped: contributes +0.0, bitwise neutral -- rows.cuh) and
+// updates the row as k_l1_sweep does, so the result is bitwise the
+// multi-launch one.
+static inline size_t coarse_smem(const amgp_mat *A) {
+    return 16 * (size_t)A->nrows + 12 * (size_t)A->stored + 64;
+}
+
 __global__ void __launch_bounds__(1024)
 k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__ b,
             double *__restrict__ x, int sweeps) {
@@ -110,8 +109,7 @@ k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__
     const int64_t stored = A.slice_ptr[A.nslices];
     double *buf[2] = {sh, sh + n};
     double *pv = sh + 2 * n;
-    double *prod = pv + stored;
-    int32_t *pc = (int32_t *)(prod + (PROD ? stored : 0));
+    int32_t *pc = (int32_t *)(pv + stored);
     for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
         pv[e] = A.val[e];
         pc[e] = A.col[e];
@@ -120,10 +118,64 @@ k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__
     for (int s = 1; s <= sweeps; s++) {
         const double *xin = buf[(s - 1) & 1];
         double *xout = buf[s & 1];
-        if (PROD && s > 1) {
-            for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
-                const int32_t c = pc[e];
-                prod[e] = c >= 0 ? __dmul_rn(pv[e], xin[c]) : 0.0;
+        for (int64_t row = threadIdx.x; row < n; row += blockDim.x) {
+            double y = 0.0;
+            if (s > 1) {
+                const int64_t sl = row >> 5;
+                const int lane = row & 31;
+                const int64_t base = A.slice_ptr[sl];
+                const int w = (int)((A.slice_ptr[sl + 1] - base) >> 5);
+                const double *vv = pv + base + lane;
+                const int32_t *cc = pc + base + lane;
+#pragma unroll 8
+                for (int j = 0; j < w; j++) {
+                    const int32_t c = cc[j * 32];
+                    if (c >= 0) y = __dadd_rn(y, __dmul_rn(vv[j * 32], xin[c]));
+                }
+            }
+            const double rr = __dsub_rn(b[row], y);
+            xout[row] = __dadd_rn(s > 1 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
+        }
+        __syncthreads();
+    }
+    for (int64_t row = threadIdx.x; row < n; row += blockDim.x) x[row] = buf[sweeps & 1][row];
+}
+
+// K6 for coarsest levels of at most COARSE_REG_SLOTS SELL slots: each of
+// the 1024 threads keeps the values of its 16 slots in registers across all
+// sweeps (16-bit columns in shared memory), so a sweep is one parallel
+// product pass over the shared-memory iterate plus the ordered row sums --
+// the same operations in the same order as k_coarse_l1.
+#define COARSE_REG_K 16
+#define COARSE_REG_SLOTS (1024 * COARSE_REG_K)
+__global__ void __launch_bounds__(1024, 1)
+k_coarse_l1_reg(SellView A, const double *__restrict__ m, const double *__restrict__ b,
+                double *__restrict__ x, int sweeps) {
+    extern __shared__ double sh[];
+    const int64_t n = A.nrows;
+    const int stored = (int)A.slice_ptr[A.nslices];
+    double *buf[2] = {sh, sh + n};
+    double *prod = sh + 2 * n;
+    int16_t *pc = (int16_t *)(prod + stored);  // 16-bit columns (ncols < 32768)
+    double vr[COARSE_REG_K];
+#pragma unroll
+    for (int k = 0; k < COARSE_REG_K; k++) {
+        const int e = threadIdx.x + k * 1024;
+        if (e < stored) pc[e] = (int16_t)A.col[e];
+        vr[k] = e < stored ? A.val[e] : 0.0;
+    }
+    __syncthreads();
+    for (int s = 1; s <= sweeps; s++) {
+        const double *xin = buf[(s - 1) & 1];
+        double *xout = buf[s & 1];
+        if (s > 1) {
+#pragma unroll
+            for (int k = 0; k < COARSE_REG_K; k++) {
+                const int e = threadIdx.x + k * 1024;
+                if (e < stored) {
+                    const int c = pc[e];
+                    prod[e] = c >= 0 ? __dmul_rn(vr[k], xin[c]) : 0.0;
+                }
             }
             __syncthreads();
         }
@@ -134,22 +186,12 @@ k_coarse_l1(SellView A, const double *__restrict__ m, const double *__restrict__
                 const int lane = row & 31;
                 const int64_t base = A.slice_ptr[sl];
                 const int w = (int)((A.slice_ptr[sl + 1] - base) >> 5);
-                if (PROD) {
-                    const double *pp = prod + base + lane;
+                const double *pp = prod + base + lane;
 #pragma unroll 8
-                    for (int j = 0; j < w; j++) y = __dadd_rn(y, pp[j * 32]);
-                } else {
-                    const double *vv = pv + base + lane;
-                    const int32_t *cc = pc + base + lane;
-#pragma unroll 8
-                    for (int j = 0; j < w; j++) {
-                        const int32_t c = cc[j * 32];
-                        if (c >= 0) y = __dadd_rn(y, __dmul_rn(vv[j * 32], xin[c]));
-                    }
-                }
+                for (int j = 0; j < w; j++) y = __dadd_rn(y, pp[j * 32]);
             }
-            const double rr = __dsub_rn(b[row], y);
-            xout[row] = __dadd_rn(s > 1 ? xin[row] : 0.0, __ddiv_rn(rr, m[row]));
+            const double rr = __dsub_rn(__ldg(b + row), y);
+            xout[row] = __dadd_rn(s > 1 ? xin[row] : 0.0, __ddiv_rn(rr, __ldg(m + row)));
         }
         __syncthreads();
     }
@@ -201,15 +243,14 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
     }
     if (h->coarse_solver == AMGP_COARSE_SMOOTHER)
         return smoother_enqueue(ctx, A, h->m[l], h->plan[l], r, nullptr, z, h->work[l]);
-    if (!A->halo && coarse_smem(A, true) <= COARSE_SMEM_BYTES) {
-        k_coarse_l1<true><<<1, 1024, coarse_smem(A, true), ctx->stream>>>(view_of(A), h->m[l], r, z,
-                                                                           h->coarse_sweeps);
+    const size_t reg_smem = 16 * (size_t)A->nrows + 10 * (size_t)A->stored + 64;
+    if (!A->halo && A->stored <= COARSE_REG_SLOTS && A->ncols < 32768 && reg_smem <= COARSE_SMEM_BYTES) {
+        k_coarse_l1_reg<<<1, 1024, reg_smem, ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
-    if (!A->halo && coarse_smem(A, false) <= COARSE_SMEM_BYTES) {
-        k_coarse_l1<false><<<1, 1024, coarse_smem(A, false), ctx->stream>>>(view_of(A), h->m[l], r, z,
-                                                                            h->coarse_sweeps);
+    if (!A->halo && coarse_smem(A) <= COARSE_SMEM_BYTES) {
+        k_coarse_l1<<<1, 1024, coarse_smem(A), ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
@@ -438,7 +479,7 @@ static void tail_plan(amgp_hier *h) {
     if (!h->use_tail || h->coarse_solver != AMGP_COARSE_L1_JACOBI) return;
     const int Lc = h->nlev - 1;
     amgp_mat *C = h->A[Lc];
-    if (C->halo || coarse_smem(C, true) > TAIL_COARSE_SMEM || C->nrows > TAIL_MAX_ROWS) return;
+    if (C->halo || tail_coarse_smem(C) > TAIL_COARSE_SMEM || C->nrows > TAIL_MAX_ROWS) return;
     int start = Lc;
     for (int l = Lc - 1; l >= 0 && Lc - l < TAIL_MAX_LEV; l--) {
         const amgp_mat *A = h->A[l];
@@ -487,7 +528,7 @@ static int tail_prepare(amgp_hier *h) {
     if (!h->d_tail) AMGP_CUDA(cudaMalloc(&h->d_tail, sizeof(TailDesc)));
     AMGP_CUDA(cudaStreamSynchronize(h->ctx->stream));
     AMGP_CUDA(cudaMemcpy(h->d_tail, &d, sizeof(TailDesc), cudaMemcpyHostToDevice));
-    h->tail_smem = std::max<size_t>((size_t)TAIL_CHUNK * 32 * sizeof(double), coarse_smem(h->A[h->nlev - 1], true));
+    h->tail_smem = std::max<size_t>((size_t)TAIL_CHUNK * 32 * sizeof(double), tail_coarse_smem(h->A[h->nlev - 1]));
     AMGP_CUDA(cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)h->tail_smem));
     int per_sm = 0, nsm = 0;
@@ -635,9 +676,9 @@ extern "C" int amgp_hier_create(amgp_ctx *ctx, int nlevels, amgp_mat *const *A,
         return amgp_cuda_fail(e, "hierarchy buffers", __FILE__, __LINE__);
     }
     // K6 stages the coarsest level in up to 227 KB of dynamic shared memory
-    cudaFuncSetAttribute(k_coarse_l1<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_coarse_l1, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          COARSE_SMEM_BYTES);
-    cudaFuncSetAttribute(k_coarse_l1<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_coarse_l1_reg, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          COARSE_SMEM_BYTES);
     cudaFuncSetAttribute(k_chol_solve, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     *out = h;

@@ -486,11 +486,12 @@ def test_single_reduction_pcg_iterations(P, kind):
     assert np.linalg.norm(np.ones(40) - T.to_dense() @ x) / np.sqrt(40) <= 1e-9
 
 
-@pytest.mark.parametrize("nc", [40, 121])
-def test_coarse_solve_shared_memory_variants_bitwise(P, nc):
-    """Coarsest-level l1 sweeps in one CTA: nc = 40 stages the slot products
-    in shared memory, nc = 121 (dense, 311 KB with products) forms them per
-    row from the staged slots -- both bitwise equal to the oracle V-cycle."""
+@pytest.mark.parametrize("nc,band", [(40, None), (121, None), (300, 27)])
+def test_coarse_solve_shared_memory_variants_bitwise(P, nc, band):
+    """Coarsest-level l1 sweeps in one CTA.  nc = 40 and the dense nc = 121
+    (15,488 SELL slots) keep the slot values in registers; nc = 300 with 55
+    entries per row (17,600 slots) stages values and columns in shared
+    memory -- both bitwise equal to the oracle V-cycle."""
     import scipy.sparse as sp
 
     A0, _ = P.poisson3d(11)
@@ -499,7 +500,12 @@ def test_coarse_solve_shared_memory_variants_bitwise(P, nc):
     agg = np.minimum(np.arange(n0) * nc // n0, nc - 1)
     Pm = sp.csr_matrix((rng.uniform(0.5, 1.5, n0), (np.arange(n0), agg)), shape=(n0, nc))
     B = rng.standard_normal((nc, nc))
-    A1 = sp.csr_matrix(B @ B.T + nc * np.eye(nc))
+    D1 = B @ B.T
+    if band is not None:
+        i, j = np.indices((nc, nc))
+        D1[np.abs(i - j) > band] = 0.0
+        D1 += np.diag(np.abs(D1).sum(axis=1))
+    A1 = sp.csr_matrix(D1 + nc * np.eye(nc))
 
     def csr(M):
         M = sp.csr_matrix(M)

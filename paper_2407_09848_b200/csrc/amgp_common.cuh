@@ -67,15 +67,26 @@ struct amgp_ctx {
     cudaStream_t comm_stream = nullptr;
     cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
     double *gather_buf = nullptr;  // allgather scratch for global dots
-    // direct NVLink transport (AMGP_HALO=p2p): peers' halo buffers and flag
-    // words mapped through CUDA IPC; stream memory operations order them
-    int halo_p2p = 0;
-    uint32_t *flags = nullptr;         // [AMGP_MAX_SLOTS][nranks][2] ready / consumed
-    std::vector<uint32_t *> peer_flags;  // every rank's flag array (self included)
+    // direct NVLink transport (AMGP_HALO=p2p, dist.cu): peers' halo buffers
+    // and synchronisation words mapped through CUDA IPC; the kernels
+    // themselves signal and wait (sync_stride words per matrix slot)
+    int halo_p2p = 0;  // 0: NCCL, 1: p2p (default), -1: diagnostic AMGP_HALO=skip (no transfer)
+    unsigned long long *sync = nullptr;            // [AMGP_MAX_SLOTS][sync_stride]
+    std::vector<unsigned long long *> peer_sync;   // every rank's sync array (self included)
+    int sync_stride = 0;
     int next_slot = 0;
+    // AMGP_P2P_FUSED=1: one launch per distributed SpMV (pack inline, boundary
+    // CTAs wait in-kernel) -- correct but slower than the default two launches
+    int p2p_fused = 0;
 };
 
 #define AMGP_MAX_SLOTS 256
+// per-slot synchronisation words of the p2p transport (u64, monotonic):
+//   [0, nranks)         ready[src]    -- epoch of the last halo src delivered here
+//   [nranks, 2 nranks)  consumed[dst] -- epoch whose halo dst has finished reading
+//   [2 nranks]          epoch         -- exchanges completed on this rank
+//   [2 nranks + 1]      ticket        -- pack-kernel CTAs done (last one signals)
+//   [2 nranks + 2]      ticket        -- fused SpMV CTAs done (last one completes)
 
 // Halo plan of a row-distributed matrix (dist.cu).  Columns [0, nown) are
 // the rank's own entries of the operand vector; columns >= nown index the
@@ -95,11 +106,16 @@ struct HaloPlan {
     // run, boundary = the two block ends) kernels index slices directly
     // instead of through the list
     std::vector<std::pair<int64_t, int64_t>> interior_runs, boundary_runs;
-    // p2p transport: flag slot, per-peer remote destinations of my data
+    // p2p transport: sync slot, per-peer remote destinations of my data
     int slot = -1;
     double **d_dest = nullptr;       // device [npeers] remote base for my segment
     int64_t *d_seg = nullptr;        // device [npeers + 1] send offsets
     std::vector<void *> opened;      // IPC-opened peer halo allocations
+    unsigned long long *sync_slot = nullptr;  // device: this slot's words on this rank
+    int *d_sendp = nullptr, *d_recvp = nullptr;  // device: ranks I send to / receive from
+    int nsendp = 0, nrecvp = 0;
+    unsigned long long **d_ready_remote = nullptr;     // [nsendp] ready[me] on each receiver
+    unsigned long long **d_consumed_remote = nullptr;  // [nrecvp] consumed[me] on each sender
 };
 
 struct amgp_mat {
@@ -120,28 +136,103 @@ struct amgp_mat {
 };
 
 // Plain-old-data view passed to kernels.
+#define SELL_RUNS 8
 struct SellView {
     const int64_t *__restrict__ slice_ptr;
     const int32_t *__restrict__ col;
     const double *__restrict__ val;
     int64_t nrows;
     int64_t nslices;
-    const int32_t *__restrict__ slist;  // slices to process (nullptr: s0 .. s0+nlist-1)
+    const int32_t *__restrict__ slist;  // slices to process (nullptr: the run table)
     int64_t nlist;
     int64_t nown;                       // gathers of columns >= nown read xh
     const double *__restrict__ xh;
-    int64_t s0;                         // first slice of a contiguous run
+    // up to SELL_RUNS runs of consecutive slices: launch index i < run_end[0]
+    // is slice run_s0[0] + i, etc. (interior / boundary sets of row blocks)
+    int nruns;
+    int64_t run_s0[SELL_RUNS], run_end[SELL_RUNS];
+    // p2p transport: before gathering xh, wait until every rank in recvp has
+    // delivered this exchange (sync words of the matrix slot, amgp_ctx);
+    // fused launches: indices < nfirst are interior slices, and the last CTA
+    // signals consumed_remote (halo_complete)
+    unsigned long long *sync_slot;
+    const int *recvp;
+    int nrecvp, nranks;
+    int fused;
+    int64_t nfirst;
+    unsigned long long *const *consumed_remote;
 };
 
 inline SellView view_of(const amgp_mat *A) {
-    return SellView{A->slice_ptr, A->col, A->val, A->nrows, A->nslices,
-                    nullptr,      A->nslices, INT64_MAX, nullptr, 0};
+    SellView v{};
+    v.slice_ptr = A->slice_ptr;
+    v.col = A->col;
+    v.val = A->val;
+    v.nrows = A->nrows;
+    v.nslices = A->nslices;
+    v.nlist = A->nslices;
+    v.nown = INT64_MAX;
+    v.nruns = 1;
+    v.run_s0[0] = 0;
+    v.run_end[0] = A->nslices;
+    return v;
+}
+
+// slice processed by launch index idx (run table; see SellView)
+__device__ __forceinline__ int64_t run_slice(const SellView &A, int64_t idx) {
+    int64_t s = A.run_s0[0] + idx;
+#pragma unroll
+    for (int r = 1; r < SELL_RUNS; r++)
+        if (r < A.nruns && idx >= A.run_end[r - 1]) s = A.run_s0[r] + (idx - A.run_end[r - 1]);
+    return s;
+}
+
+// system-scope acquire / release on u64 words (peer-mapped synchronisation)
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
+    unsigned long long v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned long long v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+// Boundary kernels of the p2p transport: one thread per CTA waits until the
+// halo of the current exchange (epoch + 1) has arrived from every sender.
+__device__ __forceinline__ void halo_wait(const SellView &A) {
+    if (A.nrecvp == 0) return;
+    if (threadIdx.x == 0) {
+        const unsigned long long e = ld_acquire_sys(A.sync_slot + 2 * A.nranks) + 1;
+        for (int i = 0; i < A.nrecvp; i++)
+            while (ld_acquire_sys(A.sync_slot + A.recvp[i]) < e) __nanosleep(20);
+    }
+    __syncthreads();
+}
+
+// End of a fused p2p launch, called by the nctas CTAs that waited for the
+// halo: the last of them advances the epoch and tells every sender its halo
+// has been read (all reads precede the ticket; interior CTAs neither wait
+// nor count, so the ticket costs one atomic per boundary CTA).
+__device__ __forceinline__ void halo_complete(const SellView &A, unsigned nctas) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned long long *sync = A.sync_slot;
+        __threadfence();
+        unsigned long long *ticket = sync + 2 * A.nranks + 2;
+        if (atomicAdd(ticket, 1ull) == nctas - 1) {
+            *ticket = 0;
+            const unsigned long long e = sync[2 * A.nranks] + 1;
+            sync[2 * A.nranks] = e;
+            __threadfence_system();
+            for (int i = 0; i < A.nrecvp; i++) st_release_sys(A.consumed_remote[i], e);
+        }
+    }
 }
 
 // Exchange the halo of operand x (own part) for a distributed matrix; after
 // it, kernels may gather x through view.xh (dist.cu).
-int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x);
-int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A);
+int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x, bool inline_pack = false);
+int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A, bool inline_pack = false);
 int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A);  // after the boundary rows
 void mat_free_halo(amgp_mat *A);
 int refresh_slice_maxcol(amgp_mat *A);  // recompute A->slice_maxcol from the device columns

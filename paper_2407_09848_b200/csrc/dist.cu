@@ -10,7 +10,6 @@
 // [nown, nown + nhalo) = the halo buffer, filled by one grouped
 // ncclSend/ncclRecv per SpMV.  Row arithmetic does not change with the
 // partition, so every kernel returns the single-GPU bits.
-#include <cuda.h>
 #include <dlfcn.h>
 #include <nccl.h>
 #include <stdio.h>
@@ -25,36 +24,18 @@
 // ---------------------------------------------------------------- direct NVLink transport
 // AMGP_HALO=p2p: instead of NCCL send/recv, the pack kernel stores each
 // neighbour's halo entries straight into the neighbour's halo buffer (CUDA
-// IPC mapping, NVLink stores), and stream memory operations hand over
-// ownership: the sender waits until the receiver has consumed the previous
-// exchange, writes, then sets the receiver's "ready" word; the receiver's
-// stream waits on "ready" before its boundary rows and sets the sender's
-// "consumed" word after them.  No communication kernel, no proxy thread;
-// the waits are done by the stream front end (no spinning kernels).
-typedef CUresult (*PFN_streamValue32)(CUstream, CUdeviceptr, cuuint32_t, unsigned int);
-static PFN_streamValue32 g_wait32 = nullptr, g_write32 = nullptr;
-
-static int load_stream_memops() {
-    if (g_wait32 && g_write32) return AMGP_OK;
-    cudaDriverEntryPointQueryResult q1, q2;
-    AMGP_CUDA(cudaGetDriverEntryPoint("cuStreamWaitValue32", (void **)&g_wait32, cudaEnableDefault, &q1));
-    AMGP_CUDA(cudaGetDriverEntryPoint("cuStreamWriteValue32", (void **)&g_write32, cudaEnableDefault, &q2));
-    if (!g_wait32 || !g_write32 || q1 != cudaDriverEntryPointSuccess || q2 != cudaDriverEntryPointSuccess)
-        return amgp_fail(AMGP_ECUDA, "stream memory operations unavailable");
-    return AMGP_OK;
-}
-
-#define CU_TRY(call)                                                                      \
-    do {                                                                                  \
-        CUresult _r = (call);                                                             \
-        if (_r != CUDA_SUCCESS)                                                           \
-            return amgp_fail(AMGP_ECUDA, "driver call failed (CUresult " + std::to_string((int)_r) + "): " #call); \
-    } while (0)
-
-static inline CUdeviceptr flag_addr(uint32_t *base, int slot, int nranks, int peer, int which) {
-    return (CUdeviceptr)(base + ((size_t)slot * nranks + peer) * 2 + which);
-}
-
+// IPC mapping, NVLink stores) and the kernels hand over ownership through
+// monotonic u64 epoch words (amgp_ctx::sync, one slot per distributed
+// matrix, peer-mapped):
+//   pack (comm stream)  waits consumed[dst] >= epoch (dst finished reading the
+//                       previous exchange), stores, and its last CTA sets
+//                       ready[me] = epoch + 1 on every receiver (release.sys)
+//   boundary rows       wait ready[src] >= epoch + 1 (acquire.sys) first
+//   completion          epoch += 1 and consumed[me] = epoch on every sender:
+//                       the last CTA of the fused interior+boundary launch
+//                       (rows.cuh ROWS_FUSED), else k_halo_signal
+// Exchange order is the same on every rank (SPMD), so no wait can close a
+// cycle; everything is an ordinary kernel and is captured into graphs.
 struct NcclApi {
     bool ok = false;
     ncclResult_t (*GetUniqueId)(ncclUniqueId *) = nullptr;
@@ -132,30 +113,48 @@ static int allgather_host(amgp_ctx *ctx, const void *mine, size_t bytes, std::ve
     return AMGP_OK;
 }
 
+// Map every rank's synchronisation words.  Collective; when any rank cannot
+// map a peer (no CUDA IPC / peer access between the GPUs) every rank stays
+// on NCCL.
 static int p2p_init(amgp_ctx *ctx) {
-    AMGP_TRY(load_stream_memops());
     const int nr = ctx->nranks;
-    const size_t nflags = (size_t)AMGP_MAX_SLOTS * nr * 2;
-    AMGP_CUDA(cudaMalloc(&ctx->flags, nflags * sizeof(uint32_t)));
-    std::vector<uint32_t> init(nflags, 0);
-    for (size_t i = 1; i < nflags; i += 2) init[i] = 1;  // every halo buffer starts consumed
-    AMGP_CUDA(cudaMemcpy(ctx->flags, init.data(), nflags * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    ctx->sync_stride = 2 * nr + 3;
+    const size_t words = (size_t)AMGP_MAX_SLOTS * ctx->sync_stride;
+    AMGP_CUDA(cudaMalloc(&ctx->sync, words * sizeof(unsigned long long)));
+    AMGP_CUDA(cudaMemset(ctx->sync, 0, words * sizeof(unsigned long long)));
     cudaIpcMemHandle_t mine;
-    AMGP_CUDA(cudaIpcGetMemHandle(&mine, ctx->flags));
+    AMGP_CUDA(cudaIpcGetMemHandle(&mine, ctx->sync));
     std::vector<char> all;
     AMGP_TRY(allgather_host(ctx, &mine, sizeof(mine), all));
-    ctx->peer_flags.assign(nr, nullptr);
+    ctx->peer_sync.assign(nr, nullptr);
+    int ok = 1;
     for (int r = 0; r < nr; r++) {
         if (r == ctx->rank) {
-            ctx->peer_flags[r] = ctx->flags;
+            ctx->peer_sync[r] = ctx->sync;
             continue;
         }
         cudaIpcMemHandle_t h;
         memcpy(&h, all.data() + r * sizeof(h), sizeof(h));
         void *p = nullptr;
-        AMGP_CUDA(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess));
-        ctx->peer_flags[r] = (uint32_t *)p;
+        if (cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = 0;
+            continue;
+        }
+        ctx->peer_sync[r] = (unsigned long long *)p;
     }
+    std::vector<char> oks;
+    AMGP_TRY(allgather_host(ctx, &ok, sizeof(ok), oks));
+    for (int r = 0; r < nr; r++) ok &= ((const int *)oks.data())[r];
+    if (!ok) {
+        for (int r = 0; r < nr; r++)
+            if (r != ctx->rank && ctx->peer_sync[r]) cudaIpcCloseMemHandle(ctx->peer_sync[r]);
+        ctx->peer_sync.clear();
+        cudaFree(ctx->sync);
+        ctx->sync = nullptr;
+        return AMGP_OK;  // halo_p2p stays 0: NCCL transport
+    }
+    AMGP_CUDA(cudaDeviceSynchronize());
     ctx->halo_p2p = 1;
     return AMGP_OK;
 }
@@ -182,10 +181,15 @@ extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const cha
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_exchanged, cudaEventDisableTiming));
     AMGP_CUDA(cudaMalloc(&ctx->gather_buf, (size_t)nranks * 16 * sizeof(double)));
+    // halo transport: direct NVLink (default when every pair of GPUs can
+    // map each other, <= 64 ranks) or NCCL (AMGP_HALO=nccl, or fallback)
     const char *mode = getenv("AMGP_HALO");
-    if (mode && strcmp(mode, "p2p") == 0 && nranks > 1) {
-        if (nranks > 64) return amgp_fail(AMGP_EINVAL, "p2p halo transport supports <= 64 ranks");
+    if (mode && strcmp(mode, "skip") == 0) ctx->halo_p2p = -1;  // diagnostic: no transfer (stale halo)
+    const bool want_p2p = !mode || strcmp(mode, "p2p") == 0;
+    if (want_p2p && nranks > 1 && nranks <= 64) {
         AMGP_TRY(p2p_init(ctx));
+        const char *fz = getenv("AMGP_P2P_FUSED");
+        ctx->p2p_fused = fz ? atoi(fz) : 0;
     }
     return AMGP_OK;
 }
@@ -203,6 +207,10 @@ static void halo_free(HaloPlan *h) {
     for (void *p : h->opened) cudaIpcCloseMemHandle(p);
     cudaFree(h->d_dest);
     cudaFree(h->d_seg);
+    cudaFree(h->d_sendp);
+    cudaFree(h->d_recvp);
+    cudaFree(h->d_ready_remote);
+    cudaFree(h->d_consumed_remote);
     cudaFree(h->send_idx);
     cudaFree(h->sendbuf);
     cudaFree(h->halo);
@@ -254,6 +262,34 @@ static int p2p_attach(amgp_ctx *ctx, HaloPlan *h) {
     AMGP_CUDA(cudaMalloc(&h->d_seg, (np + 1) * sizeof(int64_t)));
     if (np) AMGP_CUDA(cudaMemcpy(h->d_dest, dest.data(), np * sizeof(double *), cudaMemcpyHostToDevice));
     AMGP_CUDA(cudaMemcpy(h->d_seg, seg.data(), (np + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
+    // synchronisation words: mine for this slot, and where to signal peers
+    const int nr = ctx->nranks, me = ctx->rank, st = ctx->sync_stride;
+    h->sync_slot = ctx->sync + (size_t)h->slot * st;
+    std::vector<int> sendp, recvp;
+    std::vector<unsigned long long *> ready_remote, consumed_remote;
+    for (size_t q = 0; q < np; q++) {
+        const int r = h->peers[q];
+        if (h->send_cnt[q] > 0) {
+            sendp.push_back(r);
+            ready_remote.push_back(ctx->peer_sync[r] + (size_t)h->slot * st + me);
+        }
+        if (h->recv_cnt[q] > 0) {
+            recvp.push_back(r);
+            consumed_remote.push_back(ctx->peer_sync[r] + (size_t)h->slot * st + nr + me);
+        }
+    }
+    h->nsendp = (int)sendp.size();
+    h->nrecvp = (int)recvp.size();
+    auto upload = [](void **dst, const void *src, size_t bytes) -> cudaError_t {
+        cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 8));
+        if (e == cudaSuccess && bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
+        return e;
+    };
+    AMGP_CUDA(upload((void **)&h->d_sendp, sendp.data(), sendp.size() * sizeof(int)));
+    AMGP_CUDA(upload((void **)&h->d_recvp, recvp.data(), recvp.size() * sizeof(int)));
+    AMGP_CUDA(upload((void **)&h->d_ready_remote, ready_remote.data(), ready_remote.size() * sizeof(void *)));
+    AMGP_CUDA(upload((void **)&h->d_consumed_remote, consumed_remote.data(),
+                     consumed_remote.size() * sizeof(void *)));
     return AMGP_OK;
 }
 
@@ -322,7 +358,7 @@ extern "C" int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const in
         halo_free(h);
         return amgp_cuda_fail(e, "halo plan upload", __FILE__, __LINE__);
     }
-    if (ctx->halo_p2p) {  // collective: every rank attaches its plans in the same order
+    if (ctx->halo_p2p > 0) {  // collective: every rank attaches its plans in the same order
         int st = p2p_attach(ctx, h);
         if (st != AMGP_OK) {
             halo_free(h);
@@ -352,67 +388,87 @@ __global__ void k_pack(int64_t n, const int64_t *__restrict__ idx, const double 
         out[i] = x[idx[i]];
 }
 
-// p2p pack: entry i of the send list goes straight to its receiver's halo
+// p2p pack: entry i of the send list goes straight to its receiver's halo.
+// Thread 0 of every CTA first waits until each receiver has consumed the
+// previous exchange; the last CTA to finish publishes the new epoch.
 __global__ void k_pack_p2p(int64_t n, int npeers, const int64_t *__restrict__ idx,
                            const double *__restrict__ x, double *const *__restrict__ dest,
-                           const int64_t *__restrict__ seg) {
+                           const int64_t *__restrict__ seg, unsigned long long *sync, int nranks,
+                           const int *__restrict__ sendp, int nsendp,
+                           unsigned long long *const *__restrict__ ready_remote) {
+    __shared__ unsigned long long epoch;
+    if (threadIdx.x == 0) {
+        epoch = ld_acquire_sys(sync + 2 * nranks);
+        for (int i = 0; i < nsendp; i++)
+            while (ld_acquire_sys(sync + nranks + sendp[i]) < epoch) __nanosleep(20);
+    }
+    __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int q = 0;
         while (q + 1 < npeers && i >= seg[q + 1]) q++;
         dest[q][i - seg[q]] = x[idx[i]];
     }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        unsigned long long *ticket = sync + 2 * nranks + 1;
+        if (atomicAdd(ticket, 1ull) == gridDim.x - 1) {
+            *ticket = 0;
+            __threadfence_system();
+            for (int i = 0; i < nsendp; i++) st_release_sys(ready_remote[i], epoch + 1);
+        }
+    }
 }
 
-static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
-    CUstream s = (CUstream)ctx->stream;
-    const int nr = ctx->nranks, me = ctx->rank;
-    for (size_t q = 0; q < h.peers.size(); q++) {  // receiver done with the previous data
-        if (h.send_cnt[q] == 0) continue;
-        const CUdeviceptr consumed = flag_addr(ctx->flags, h.slot, nr, h.peers[q], 1);
-        CU_TRY(g_wait32(s, consumed, 1, CU_STREAM_WAIT_VALUE_EQ));
-        CU_TRY(g_write32(s, consumed, 0, CU_STREAM_WRITE_VALUE_DEFAULT));
+// after the boundary rows: this exchange is complete on this rank
+__global__ void k_halo_signal(unsigned long long *sync, int nranks, int nrecvp,
+                              unsigned long long *const *__restrict__ consumed_remote) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long e = sync[2 * nranks] + 1;
+    sync[2 * nranks] = e;
+    __threadfence_system();
+    for (int i = 0; i < nrecvp; i++) st_release_sys(consumed_remote[i], e);
+}
+
+// inline: the pack runs on the compute stream ahead of a fused launch (whose
+// boundary CTAs spin, so the pack must never wait for SM slots behind them)
+static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x, bool inline_pack) {
+    if (h.nsend == 0) return AMGP_OK;
+    cudaStream_t st = inline_pack ? ctx->stream : ctx->comm_stream;
+    if (!inline_pack) {
+        AMGP_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
+        AMGP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
     }
-    if (h.nsend > 0) {
-        const unsigned g = (unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 8);
-        k_pack_p2p<<<g, 256, 0, ctx->stream>>>(h.nsend, (int)h.peers.size(), h.send_idx, x, h.d_dest,
-                                              h.d_seg);
-        AMGP_CHECK_LAUNCH(ctx);
-    }
-    for (size_t q = 0; q < h.peers.size(); q++) {  // data in place: signal (after a memory fence)
-        if (h.send_cnt[q] == 0) continue;
-        CU_TRY(g_write32(s, flag_addr(ctx->peer_flags[h.peers[q]], h.slot, nr, me, 0), 1,
-                         CU_STREAM_WRITE_VALUE_DEFAULT));
-    }
+    const unsigned g = (unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 4);
+    k_pack_p2p<<<g, 256, 0, st>>>(h.nsend, (int)h.peers.size(), h.send_idx, x, h.d_dest, h.d_seg,
+                                  h.sync_slot, ctx->nranks, h.d_sendp, h.nsendp, h.d_ready_remote);
+    AMGP_CHECK_LAUNCH(ctx);
+    if (!inline_pack) AMGP_CUDA(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
     return AMGP_OK;
 }
 
-static int p2p_end(amgp_ctx *ctx, const HaloPlan &h) {
-    CUstream s = (CUstream)ctx->stream;
-    for (size_t q = 0; q < h.peers.size(); q++) {
-        if (h.recv_cnt[q] == 0) continue;
-        const CUdeviceptr ready = flag_addr(ctx->flags, h.slot, ctx->nranks, h.peers[q], 0);
-        CU_TRY(g_wait32(s, ready, 1, CU_STREAM_WAIT_VALUE_EQ));
-        CU_TRY(g_write32(s, ready, 0, CU_STREAM_WRITE_VALUE_DEFAULT));
-    }
+static int p2p_end(amgp_ctx *ctx, const HaloPlan &h, bool inline_pack) {
+    if (inline_pack) return AMGP_OK;
+    // the pack kernel must not be overtaken by the next exchange's; the
+    // data itself is awaited inside the boundary kernels (halo_wait)
+    if (h.nsend > 0) AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
     return AMGP_OK;
 }
 
 int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A) {
-    if (!ctx->halo_p2p) return AMGP_OK;
+    if (ctx->halo_p2p <= 0) return AMGP_OK;
     const HaloPlan &h = *A->halo;
-    CUstream s = (CUstream)ctx->stream;
-    for (size_t q = 0; q < h.peers.size(); q++) {  // boundary rows read the halo: release it
-        if (h.recv_cnt[q] == 0) continue;
-        CU_TRY(g_write32(s, flag_addr(ctx->peer_flags[h.peers[q]], h.slot, ctx->nranks, ctx->rank, 1),
-                         1, CU_STREAM_WRITE_VALUE_DEFAULT));
-    }
+    if (h.peers.empty()) return AMGP_OK;
+    k_halo_signal<<<1, 32, 0, ctx->stream>>>(h.sync_slot, ctx->nranks, h.nrecvp, h.d_consumed_remote);
+    AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }
 
-int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
+int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x, bool inline_pack) {
     const HaloPlan &h = *A->halo;
-    if (ctx->halo_p2p) return p2p_begin(ctx, h, x);
+    if (ctx->halo_p2p < 0) return AMGP_OK;
+    if (ctx->halo_p2p) return p2p_begin(ctx, h, x, inline_pack);
     NcclApi *api = nccl();
     if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator for the halo exchange");
     if (h.nsend > 0) {
@@ -437,8 +493,9 @@ int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
     return AMGP_OK;
 }
 
-int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A) {
-    if (ctx->halo_p2p) return p2p_end(ctx, *A->halo);
+int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A, bool inline_pack) {
+    if (ctx->halo_p2p < 0) return AMGP_OK;
+    if (ctx->halo_p2p) return p2p_end(ctx, *A->halo, inline_pack);
     AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
     return AMGP_OK;
 }

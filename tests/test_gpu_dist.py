@@ -2,7 +2,9 @@
 
 Bitwise smoother apply on generated row blocks and bitwise V-cycles of a
 row-partitioned native hierarchy against the C oracle; distributed PCG/FCG
-iteration counts equal to the oracle's (+-1 bar).
+iteration counts equal to the oracle's (+-1 bar) -- for each halo transport:
+NCCL send/recv, the direct NVLink transport (default), and its fused
+single-launch variant.
 """
 
 import json
@@ -35,8 +37,9 @@ def free_port():
     return p
 
 
+@pytest.mark.parametrize("transport", ["nccl", "p2p", "p2p_fused"])
 @pytest.mark.parametrize("graph", [False, True])
-def test_dist_check_two_gpus(graph):
+def test_dist_check_two_gpus(graph, transport):
     if ngpus() < 2:
         pytest.skip("needs 2 GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
@@ -44,7 +47,12 @@ def test_dist_check_two_gpus(graph):
            os.path.join(REPO, "tools", "dist_check.py"), "--grid", "24"]
     if graph:
         cmd.append("--graph")
-    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    env = dict(os.environ)
+    env.pop("AMGP_P2P_FUSED", None)
+    env["AMGP_HALO"] = "nccl" if transport == "nccl" else "p2p"
+    if transport == "p2p_fused":
+        env["AMGP_P2P_FUSED"] = "1"
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == 2, p.stdout[-2000:] + p.stderr[-2000:]
     for rec in lines:

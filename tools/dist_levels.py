@@ -10,6 +10,7 @@ communication), and the exchange alone.
 """
 
 import argparse
+import ctypes
 import json
 import os
 import sys
@@ -79,8 +80,6 @@ def main():
             y = torch.empty(Ml.nrows, dtype=torch.float64, device="cuda")
 
             def graph_us(Dm):
-                import ctypes
-
                 ms = ctypes.c_double()
                 dist.barrier()
                 with c.scope():
@@ -88,7 +87,10 @@ def main():
                                                     args.reps, 1, ctypes.byref(ms)))
                 return round(ms.value * 1e3, 2)
 
+            hi = [ctypes.c_int64() for _ in range(4)]
+            N.check(N.lib().amgp_mat_halo_info(Dh.handle, *[ctypes.byref(v) for v in hi]))
             rec = {"level": l, "mat": name, "rows": Ml.nrows, "nnz": Ml.nnz,
+                   "slices_interior": hi[2].value, "slices_boundary": hi[3].value,
                    "halo": plan.nhalo if plan is not None else 0,
                    "peers": len(plan.peers) if plan is not None else 0,
                    "us_halo_graph": graph_us(Dh), "us_local_graph": graph_us(Dn)}

@@ -111,7 +111,8 @@ int amgp_mat_l1_diag(amgp_mat *A, double *m_dev);
 /* sparse.py:118-125 spmv: y = A x (device vectors). */
 int amgp_spmv(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y);
 /* Diagnostics: reps SpMVs back to back (captured in a CUDA graph when
- * use_graph), device time per SpMV in *ms (halo exchanges included). */
+ * use_graph & 1), device time per SpMV in *ms (halo exchanges included);
+ * use_graph & 2: the halo exchanges alone, without the row kernels. */
 int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y, int reps,
                     int use_graph, double *ms);
 /* sparse.py:128-139 fused_update: r -= s; d = d*(rho*rho_prev) + c*r; x += d. */

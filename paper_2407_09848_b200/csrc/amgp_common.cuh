@@ -65,6 +65,7 @@ struct amgp_ctx {
     void *comm = nullptr;  // ncclComm_t
     int nranks = 1, rank = 0;
     cudaStream_t comm_stream = nullptr;
+    int prio_high = 0;  // greatest stream priority (halo pack kernels)
     cudaEvent_t ev_packed = nullptr, ev_exchanged = nullptr;
     double *gather_buf = nullptr;  // allgather scratch for global dots
     // direct NVLink transport (AMGP_HALO=p2p, dist.cu): peers' halo buffers
@@ -159,6 +160,7 @@ struct SellView {
     const int *recvp;
     int nrecvp, nranks;
     int fused;
+    int complete;  // ROWS_GEN boundary launch of the p2p transport: last CTA completes
     int64_t nfirst;
     unsigned long long *const *consumed_remote;
 };

@@ -178,6 +178,7 @@ extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const cha
     int least = 0, greatest = 0;
     AMGP_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
     AMGP_CUDA(cudaStreamCreateWithPriority(&ctx->comm_stream, cudaStreamNonBlocking, greatest));
+    ctx->prio_high = greatest;
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_packed, cudaEventDisableTiming));
     AMGP_CUDA(cudaEventCreateWithFlags(&ctx->ev_exchanged, cudaEventDisableTiming));
     AMGP_CUDA(cudaMalloc(&ctx->gather_buf, (size_t)nranks * 16 * sizeof(double)));
@@ -440,9 +441,21 @@ static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x, bool inl
         AMGP_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
         AMGP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
     }
-    const unsigned g = (unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 4);
-    k_pack_p2p<<<g, 256, 0, st>>>(h.nsend, (int)h.peers.size(), h.send_idx, x, h.d_dest, h.d_seg,
-                                  h.sync_slot, ctx->nranks, h.d_sendp, h.nsendp, h.d_ready_remote);
+    // launched with the highest priority explicitly (kept when captured into
+    // a graph): its CTAs must be scheduled ahead of the interior rows
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 4));
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributePriority;
+    attr[0].val.priority = ctx->prio_high;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    AMGP_CUDA(cudaLaunchKernelEx(&cfg, k_pack_p2p, h.nsend, (int)h.peers.size(), (const int64_t *)h.send_idx,
+                                 (const double *)x, (double *const *)h.d_dest, (const int64_t *)h.d_seg,
+                                 h.sync_slot, ctx->nranks, (const int *)h.d_sendp, h.nsendp,
+                                 (unsigned long long *const *)h.d_ready_remote));
     AMGP_CHECK_LAUNCH(ctx);
     if (!inline_pack) AMGP_CUDA(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
     return AMGP_OK;

@@ -405,11 +405,21 @@ int prolong_add_enqueue(amgp_ctx *ctx, const amgp_mat *P, const double *xc, doub
 }
 
 // Diagnostics: reps back-to-back SpMVs (halo exchanges included for a
-// distributed matrix), captured once into a CUDA graph when use_graph, timed
-// with CUDA events on the context stream.  *ms = milliseconds per SpMV.
+// distributed matrix), captured once into a CUDA graph when use_graph & 1,
+// timed with CUDA events on the context stream.  *ms = milliseconds per
+// SpMV.  use_graph & 2: only the halo exchanges (transport latency).
+static int exchange_only(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
+    if (!A->halo) return AMGP_OK;
+    AMGP_TRY(halo_exchange_begin(ctx, A, x));
+    AMGP_TRY(halo_exchange_end(ctx, A));
+    return halo_exchange_done(ctx, A);
+}
+
 extern "C" int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y,
-                               int reps, int use_graph, double *ms) {
+                               int reps, int flags, double *ms) {
     if (!ctx || !A || reps < 1 || !ms) return amgp_fail(AMGP_EINVAL, "amgp_spmv_timed: bad argument");
+    const bool use_graph = flags & 1, xonly = flags & 2;
+    auto one = [&]() { return xonly ? exchange_only(ctx, A, x) : spmv_enqueue(ctx, A, x, y); };
     AMGP_CUDA(cudaSetDevice(ctx->device));
     cudaEvent_t e0, e1;
     AMGP_CUDA(cudaEventCreate(&e0));
@@ -419,7 +429,7 @@ extern "C" int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x
         cudaGraph_t g = nullptr;
         AMGP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
         int st = AMGP_OK;
-        for (int i = 0; i < reps && st == AMGP_OK; i++) st = spmv_enqueue(ctx, A, x, y);
+        for (int i = 0; i < reps && st == AMGP_OK; i++) st = one();
         cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
         if (st != AMGP_OK) return st;
         if (e != cudaSuccess) return amgp_cuda_fail(e, "capture", __FILE__, __LINE__);
@@ -427,14 +437,14 @@ extern "C" int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x
         cudaGraphDestroy(g);
         AMGP_CUDA(cudaGraphLaunch(exec, ctx->stream));  // warm-up
     } else {
-        AMGP_TRY(spmv_enqueue(ctx, A, x, y));
+        AMGP_TRY(one());
     }
     AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
     AMGP_CUDA(cudaEventRecord(e0, ctx->stream));
     if (use_graph) {
         AMGP_CUDA(cudaGraphLaunch(exec, ctx->stream));
     } else {
-        for (int i = 0; i < reps; i++) AMGP_TRY(spmv_enqueue(ctx, A, x, y));
+        for (int i = 0; i < reps; i++) AMGP_TRY(one());
     }
     AMGP_CUDA(cudaEventRecord(e1, ctx->stream));
     AMGP_CUDA(cudaEventSynchronize(e1));

@@ -63,6 +63,7 @@ k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
         if (row < A.nrows) epi(row, y);
     }
     if (bnd) halo_complete(A, gridDim.x - (unsigned)(A.nfirst / ROWS_SLICES));
+    if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }
 
 // NW warps, U slot loads in flight per thread: SPLIT_WARPS x SPLIT_U for
@@ -120,6 +121,7 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
         if (row < A.nrows) epi(row, sum);
     }
     if (MODE == ROWS_FUSED && halo) halo_complete(A, gridDim.x - (unsigned)A.nfirst);
+    if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }
 
 // Schedule choice: split when rows are long and there are too few slices to
@@ -224,6 +226,10 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     v.nown = h.nown;
     v.xh = h.halo;
     v.nrecvp = nrecvp;
+    if (p2p && h.n_boundary > 0) {  // the boundary launch completes the exchange itself
+        v.complete = 1;
+        return launch_set(h.boundary_runs, h.boundary, h.n_boundary);
+    }
     AMGP_TRY(launch_set(h.boundary_runs, h.boundary, h.n_boundary));
     return halo_exchange_done(ctx, A);
 }

@@ -112,8 +112,10 @@ def main():
     flat = [out["checks"]["block_l1diag"]] + list(res.values()) + list(vc.values()) + \
            [v["ok"] for v in pcg.values()]
     out["ok"] = bool(all(flat))
-    print(json.dumps(out), flush=True)
-    dist.barrier()
+    for r in range(comm.size):  # one rank at a time: whole lines on the shared stdout
+        if r == me:
+            print(json.dumps(out), flush=True)
+        dist.barrier()
     if me == 0:
         try:
             D.release_shared(path)

@@ -79,12 +79,12 @@ def main():
             x = torch.randn(Ml.ncols, dtype=torch.float64, device="cuda")
             y = torch.empty(Ml.nrows, dtype=torch.float64, device="cuda")
 
-            def graph_us(Dm):
+            def graph_us(Dm, flags=1):
                 ms = ctypes.c_double()
                 dist.barrier()
                 with c.scope():
                     N.check(N.lib().amgp_spmv_timed(c.handle, Dm.handle, N.ptr(x), N.ptr(y),
-                                                    args.reps, 1, ctypes.byref(ms)))
+                                                    args.reps, flags, ctypes.byref(ms)))
                 return round(ms.value * 1e3, 2)
 
             hi = [ctypes.c_int64() for _ in range(4)]
@@ -93,7 +93,8 @@ def main():
                    "slices_interior": hi[2].value, "slices_boundary": hi[3].value,
                    "halo": plan.nhalo if plan is not None else 0,
                    "peers": len(plan.peers) if plan is not None else 0,
-                   "us_halo_graph": graph_us(Dh), "us_local_graph": graph_us(Dn)}
+                   "us_halo_graph": graph_us(Dh), "us_local_graph": graph_us(Dn),
+                   "us_exchange_graph": graph_us(Dh, 3)}
             rows.append(rec)
     if comm.rank == 0:
         for r in rows:

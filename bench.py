@@ -161,7 +161,7 @@ def run_reference(args):
     from paper_2407_09848_b200.params import load_beta_tables, optimal_a
     from paper_2407_09848_b200.problems import poisson3d
 
-    m = args.m
+    m = args.grid
     from paper_2407_09848_b200.smoothers import l1_jacobi_diag
 
     A, _ = poisson3d(m)
@@ -363,7 +363,7 @@ def run_b200(args):
     c = N.ctx(dev)
     halo_info = None
     if ws == 1:
-        m = args.m
+        m = args.grid
         D = P.poisson3d_device(m)
     else:
         # weak scaling: a global cube with ~m^3 rows per GPU, contiguous row
@@ -371,7 +371,7 @@ def run_b200(args):
         from paper_2407_09848_b200 import dist as Dist
 
         comm = Dist.Communicator(local)
-        m = int(round(args.m * ws ** (1.0 / 3.0)))
+        m = int(round(args.grid * ws ** (1.0 / 3.0)))
         D = Dist.poisson3d_block(m, comm)
         halo_info = {"peers": len(D.halo.peers), "halo_rows": int(D.halo.recv_cnt.sum()),
                      "rows": D.nrows}
@@ -462,8 +462,8 @@ def run_b200(args):
            "h2d_bytes_per_step": len(cfgs) * 2 * n * 8, "d2h_bytes_per_step": len(cfgs) * n * 8}
 
     dsolve = None
-    if ws > 1 and args.solve_m > 0:
-        dsolve = dist_solve_bench(comm, args.solve_m, ws)
+    if ws > 1 and args.solve_grid > 0:
+        dsolve = dist_solve_bench(comm, args.solve_grid, ws)
 
     if rank == 0:
         line = {
@@ -492,9 +492,9 @@ def run_b200(args):
             "clocks": clocks,
         }
         if ws == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_baseline(args.cpu_m)
-        if ws == 1 and args.solve_m > 0:
-            line["solve"] = solve_bench(args.solve_m, cpu=not args.no_cpu_baseline)
+            line["cpu_baseline"] = cpu_baseline(args.cpu_grid)
+        if ws == 1 and args.solve_grid > 0:
+            line["solve"] = solve_bench(args.solve_grid, cpu=not args.no_cpu_baseline)
         if dsolve is not None:
             line["solve"] = dsolve
         print(json.dumps(line), flush=True)
@@ -510,10 +510,11 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--m", type=int, default=256)
-    ap.add_argument("--cpu-m", type=int, default=256)
+    # (--grid, not --m: torchrun's parser would take --m for its own options)
+    ap.add_argument("--grid", type=int, default=256, help="fine-level cube edge per GPU (weak-scaled for N > 1)")
+    ap.add_argument("--cpu-grid", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--solve-m", type=int, default=128,
+    ap.add_argument("--solve-grid", type=int, default=128,
                     help="grid size of the PCG+AMG solve section (0: skip)")
     args = ap.parse_args()
     if args.warmup < 3:

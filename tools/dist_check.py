@@ -1,7 +1,7 @@
 #!/usr/bin/env python
 """Multi-GPU parity check (run under torchrun, one process per GPU).
 
-    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/dist_check.py [--m 32]
+    torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/dist_check.py [--grid 32]
 
 Compares on every rank, against the C oracle on the global problem:
   1. fine-level smoother apply on a generated row block (halo-exchanged

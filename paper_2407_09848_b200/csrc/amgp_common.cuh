@@ -245,6 +245,7 @@ int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x, bool 
 int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A, bool inline_pack = false);
 int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A);  // after the boundary rows
 void mat_free_halo(amgp_mat *A);
+void ctx_free_comm(amgp_ctx *ctx);  // communicator resources (amgp_ctx_destroy)
 int refresh_slice_maxcol(amgp_mat *A);  // recompute A->slice_maxcol from the device columns
 
 // Resolved smoother configuration with host-computed step scalars

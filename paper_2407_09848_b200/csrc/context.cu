@@ -62,6 +62,7 @@ int amgp_ctx_destroy(amgp_ctx *c) {
     if (!c) return AMGP_OK;
     cudaSetDevice(c->device);
     cudaStreamSynchronize(c->stream);
+    ctx_free_comm(c);
     cudaFree(c->red_partial);
     cudaFree(c->scalars);
     cudaFreeHost(c->host_scalars);

@@ -195,6 +195,29 @@ extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const cha
     return AMGP_OK;
 }
 
+// Release the communicator side of a context (amgp_ctx_destroy): IPC
+// mappings of the peers' synchronisation words, NCCL communicator, streams.
+void ctx_free_comm(amgp_ctx *ctx) {
+    for (size_t r = 0; r < ctx->peer_sync.size(); r++)
+        if ((int)r != ctx->rank && ctx->peer_sync[r]) cudaIpcCloseMemHandle(ctx->peer_sync[r]);
+    ctx->peer_sync.clear();
+    cudaFree(ctx->sync);
+    ctx->sync = nullptr;
+    cudaFree(ctx->gather_buf);
+    ctx->gather_buf = nullptr;
+    if (ctx->ev_packed) cudaEventDestroy(ctx->ev_packed);
+    if (ctx->ev_exchanged) cudaEventDestroy(ctx->ev_exchanged);
+    ctx->ev_packed = ctx->ev_exchanged = nullptr;
+    if (ctx->comm_stream) {
+        cudaStreamSynchronize(ctx->comm_stream);
+        cudaStreamDestroy(ctx->comm_stream);
+        ctx->comm_stream = nullptr;
+    }
+    NcclApi *api = nccl();
+    if (ctx->comm && api && api->CommDestroy) api->CommDestroy((ncclComm_t)ctx->comm);
+    ctx->comm = nullptr;
+}
+
 extern "C" int amgp_ctx_comm_info(amgp_ctx *ctx, int *nranks, int *rank) {
     if (!ctx) return amgp_fail(AMGP_EINVAL, "null context");
     if (nranks) *nranks = ctx->nranks;

@@ -21,7 +21,6 @@
 #include "../../include/amgp.h"
 
 #define AMGP_SLICE 32  // SELL slice height == warp width
-#define UCOL_NONE INT32_MIN  // amgp_mat::ucol marker of a non-uniform slice
 
 // ---------------------------------------------------------------- errors
 void amgp_set_error(const std::string &msg);
@@ -130,11 +129,6 @@ struct amgp_mat {
     int32_t max_width = 0;
     int64_t row_offset = 0;  // first global row of a generated row block
     std::vector<int64_t> slice_maxcol;  // host: largest column per slice (-1: empty)
-    // device [stored / 32], one int per slot: for a *uniform* slice (slot j
-    // holds columns c_j + lane for all 32 rows -- stencil rows in natural
-    // order) ucol[slice_ptr[s]/32 + j] = c_j, so sell_row_dot streams w ints
-    // per slice instead of 32 w; first entry UCOL_NONE for other slices
-    int32_t *ucol = nullptr;
     HaloPlan *halo = nullptr;           // non-null: distributed operand
     // per-matrix smoother workspace (r, two operand buffers, x copy)
     double *work = nullptr;
@@ -148,7 +142,6 @@ struct SellView {
     const int64_t *__restrict__ slice_ptr;
     const int32_t *__restrict__ col;
     const double *__restrict__ val;
-    const int32_t *__restrict__ ucol;  // compact columns of uniform slices (amgp_mat::ucol)
     int64_t nrows;
     int64_t nslices;
     const int32_t *__restrict__ slist;  // slices to process (nullptr: the run table)
@@ -177,7 +170,6 @@ inline SellView view_of(const amgp_mat *A) {
     v.slice_ptr = A->slice_ptr;
     v.col = A->col;
     v.val = A->val;
-    v.ucol = A->ucol;
     v.nrows = A->nrows;
     v.nslices = A->nslices;
     v.nlist = A->nslices;
@@ -322,13 +314,7 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
                                                const double *__restrict__ x) {
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
-    // uniform slice: the warp streams the slice's w compact columns (a
-    // broadcast load per slot) and each lane adds its offset
-    const int32_t *uc = A.ucol ? A.ucol + (base >> 5) : nullptr;
-    const bool uni = uc && w > 0 && __ldg(uc) != UCOL_NONE;
-    const int32_t *c = uni ? uc : A.col + base + lane;
-    const int64_t cstride = uni ? 1 : AMGP_SLICE;
-    const int32_t cadd = uni ? lane : 0;
+    const int32_t *c = A.col + base + lane;
     const double *v = A.val + base + lane;
     const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
     double sum = 0.0;
@@ -338,7 +324,7 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const bool ok = j + u < w;
-            cc[u] = ok ? ld_stream_s32(c + (int64_t)(j + u) * cstride, pf) + cadd : -1;
+            cc[u] = ok ? ld_stream_s32(c + (int64_t)(j + u) * AMGP_SLICE, pf) : -1;
             vv[u] = ok ? ld_stream_f64(v + (int64_t)(j + u) * AMGP_SLICE, pf) : 0.0;
         }
 #pragma unroll

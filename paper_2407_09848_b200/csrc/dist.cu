@@ -578,36 +578,22 @@ __global__ void k_localize(int64_t stored, int32_t *col, int64_t own_lo, int64_t
     }
 }
 
-// per slice: largest column, and the compact columns of a uniform slice
-__global__ void k_slice_maxcol(SellView A, int64_t *out, int32_t *ucol, int *bad) {
+__global__ void k_slice_maxcol(SellView A, int64_t *out, int *bad) {
     const int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     const int lane = threadIdx.x & 31;
     if (s >= A.nslices) return;
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
     int64_t mx = -1;
-    bool same = true;
     for (int j = 0; j < w; j++) {
         const int32_t c = A.col[base + (int64_t)j * 32 + lane];
         if (c == -2) atomicExch(bad, 1);
         mx = max(mx, (int64_t)c);
-        const int32_t c0 = __shfl_sync(0xffffffffu, c, 0);
-        same = same && c0 >= 0 && (int64_t)c == (int64_t)c0 + lane;
     }
     for (int o = 16; o > 0; o >>= 1) mx = max(mx, (int64_t)__shfl_xor_sync(0xffffffffu, (long long)mx, o));
-    same = __all_sync(0xffffffffu, same);
     if (lane == 0) out[s] = mx;
-    if (w > 0) {
-        int32_t *uc = ucol + (base >> 5);
-        if (!same) {
-            if (lane == 0) uc[0] = UCOL_NONE;
-        } else {
-            for (int j = lane; j < w; j += 32) uc[j] = A.col[base + (int64_t)j * 32];
-        }
-    }
 }
 
-// (also refreshes the compact columns of uniform slices, amgp_mat::ucol)
 int refresh_slice_maxcol(amgp_mat *A) {
     amgp_ctx *ctx = A->ctx;
     A->slice_maxcol.assign(A->nslices, -1);
@@ -617,10 +603,7 @@ int refresh_slice_maxcol(amgp_mat *A) {
     AMGP_CUDA(cudaMalloc(&d, A->nslices * sizeof(int64_t)));
     AMGP_CUDA(cudaMalloc(&bad, sizeof(int)));
     AMGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
-    if (!A->ucol) AMGP_CUDA(cudaMalloc(&A->ucol, std::max<int64_t>(A->stored / 32, 1) * sizeof(int32_t)));
-    SellView v = view_of(A);
-    v.ucol = nullptr;
-    k_slice_maxcol<<<grid_for(A->nslices * 32, 256), 256, 0, ctx->stream>>>(v, d, A->ucol, bad);
+    k_slice_maxcol<<<grid_for(A->nslices * 32, 256), 256, 0, ctx->stream>>>(view_of(A), d, bad);
     AMGP_CHECK_LAUNCH(ctx);
     int hbad = 0;
     AMGP_CUDA(cudaMemcpyAsync(A->slice_maxcol.data(), d, A->nslices * sizeof(int64_t),

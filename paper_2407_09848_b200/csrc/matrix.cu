@@ -102,8 +102,12 @@ extern "C" int amgp_mat_from_csr(amgp_ctx *ctx, int64_t nrows, int64_t ncols,
     amgp_mat *A = nullptr;
     AMGP_TRY(mat_alloc(ctx, nrows, ncols, row_ptr[nrows], ns, stored, &A));
     int32_t wmax = 0;
-    for (int64_t s = 0; s < ns; s++)
+    A->slice_maxcol.assign(ns, -1);
+    for (int64_t s = 0; s < ns; s++) {
         wmax = std::max<int32_t>(wmax, (int32_t)((sp[s + 1] - sp[s]) / AMGP_SLICE));
+        for (int64_t e = sp[s]; e < sp[s + 1]; e++)
+            A->slice_maxcol[s] = std::max<int64_t>(A->slice_maxcol[s], col[e]);
+    }
     A->max_width = wmax;
     cudaError_t e = cudaMemcpy(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
     if (e == cudaSuccess && stored > 0)
@@ -113,11 +117,6 @@ extern "C" int amgp_mat_from_csr(amgp_ctx *ctx, int64_t nrows, int64_t ncols,
     if (e != cudaSuccess) {
         amgp_mat_destroy(A);
         return amgp_cuda_fail(e, "matrix upload", __FILE__, __LINE__);
-    }
-    int st = refresh_slice_maxcol(A);  // halo split and uniform-slice columns
-    if (st != AMGP_OK) {
-        amgp_mat_destroy(A);
-        return st;
     }
     *out = A;
     return AMGP_OK;
@@ -133,7 +132,6 @@ extern "C" int amgp_mat_destroy(amgp_mat *A) {
     cudaFree(A->slice_ptr);
     cudaFree(A->col);
     cudaFree(A->val);
-    cudaFree(A->ucol);
     cudaFree(A->work);
     delete A;
     return AMGP_OK;

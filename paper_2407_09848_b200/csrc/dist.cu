@@ -32,8 +32,12 @@
 //                       ready[me] = epoch + 1 on every receiver (release.sys)
 //   boundary rows       wait ready[src] >= epoch + 1 (acquire.sys) first
 //   completion          epoch += 1 and consumed[me] = epoch on every sender:
-//                       the last CTA of the fused interior+boundary launch
-//                       (rows.cuh ROWS_FUSED), else k_halo_signal
+//                       the boundary launch's last CTA, else k_halo_signal
+// AMGP_P2P_FUSED=1, for matrices whose slice sets are a few runs: the fused
+// launch (amgp_common.cuh "fused launch", rows.cuh ROWS_FUSED) -- pack,
+// interior, boundary and completion in ONE grid, halo double-buffered by
+// epoch parity.  Correct (GPU tests) but measured slower than the default
+// pack kernel + boundary launch.
 // Exchange order is the same on every rank (SPMD), so no wait can close a
 // cycle; everything is an ordinary kernel and is captured into graphs.
 struct NcclApi {
@@ -118,7 +122,7 @@ static int allgather_host(amgp_ctx *ctx, const void *mine, size_t bytes, std::ve
 // on NCCL.
 static int p2p_init(amgp_ctx *ctx) {
     const int nr = ctx->nranks;
-    ctx->sync_stride = 2 * nr + 3;
+    ctx->sync_stride = AMGP_SYNC_STRIDE(nr);
     const size_t words = (size_t)AMGP_MAX_SLOTS * ctx->sync_stride;
     AMGP_CUDA(cudaMalloc(&ctx->sync, words * sizeof(unsigned long long)));
     AMGP_CUDA(cudaMemset(ctx->sync, 0, words * sizeof(unsigned long long)));
@@ -256,18 +260,25 @@ static int p2p_attach(amgp_ctx *ctx, HaloPlan *h) {
         cudaIpcMemHandle_t handle;
         int64_t recv_off[64];
         int64_t recv_cnt[64];
+        int64_t nhalo;
+        int fused;
     };
     Info mine;
     memset(&mine, 0, sizeof(mine));
     AMGP_CUDA(cudaIpcGetMemHandle(&mine.handle, h->halo));
+    mine.nhalo = h->nhalo;
+    mine.fused = h->fused;
     for (size_t q = 0; q < h->peers.size(); q++) {
         mine.recv_off[h->peers[q]] = h->recv_off[q];
         mine.recv_cnt[h->peers[q]] = h->recv_cnt[q];
     }
     std::vector<char> all;
     AMGP_TRY(allgather_host(ctx, &mine, sizeof(Info), all));
+    // the fused launch changes the protocol (double buffer), so every rank
+    // must agree on it for this slot
+    for (int r = 0; r < ctx->nranks; r++) h->fused &= ((const Info *)all.data())[r].fused != 0;
     const size_t np = h->peers.size();
-    std::vector<double *> dest(np, nullptr);
+    std::vector<double *> dest(2 * np, nullptr);
     std::vector<int64_t> seg(np + 1, 0);
     for (size_t q = 0; q < np; q++) {
         seg[q] = h->send_off[q];
@@ -280,11 +291,12 @@ static int p2p_attach(amgp_ctx *ctx, HaloPlan *h) {
         AMGP_CUDA(cudaIpcOpenMemHandle(&base, peer.handle, cudaIpcMemLazyEnablePeerAccess));
         h->opened.push_back(base);
         dest[q] = (double *)base + peer.recv_off[ctx->rank];
+        dest[np + q] = dest[q] + peer.nhalo;  // parity-1 buffer
     }
     seg[np] = h->nsend;
-    AMGP_CUDA(cudaMalloc(&h->d_dest, std::max<size_t>(np, 1) * sizeof(double *)));
+    AMGP_CUDA(cudaMalloc(&h->d_dest, std::max<size_t>(2 * np, 1) * sizeof(double *)));
     AMGP_CUDA(cudaMalloc(&h->d_seg, (np + 1) * sizeof(int64_t)));
-    if (np) AMGP_CUDA(cudaMemcpy(h->d_dest, dest.data(), np * sizeof(double *), cudaMemcpyHostToDevice));
+    if (np) AMGP_CUDA(cudaMemcpy(h->d_dest, dest.data(), 2 * np * sizeof(double *), cudaMemcpyHostToDevice));
     AMGP_CUDA(cudaMemcpy(h->d_seg, seg.data(), (np + 1) * sizeof(int64_t), cudaMemcpyHostToDevice));
     // synchronisation words: mine for this slot, and where to signal peers
     const int nr = ctx->nranks, me = ctx->rank, st = ctx->sync_stride;
@@ -304,6 +316,9 @@ static int p2p_attach(amgp_ctx *ctx, HaloPlan *h) {
     }
     h->nsendp = (int)sendp.size();
     h->nrecvp = (int)recvp.size();
+    h->sym = std::all_of(sendp.begin(), sendp.end(), [&](int r) {
+        return std::find(recvp.begin(), recvp.end(), r) != recvp.end();
+    });
     auto upload = [](void **dst, const void *src, size_t bytes) -> cudaError_t {
         cudaError_t e = cudaMalloc(dst, std::max<size_t>(bytes, 8));
         if (e == cudaSuccess && bytes) e = cudaMemcpy(*dst, src, bytes, cudaMemcpyHostToDevice);
@@ -377,7 +392,11 @@ extern "C" int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const in
     up((void **)&h->interior, in.data(), in.size() * sizeof(int32_t));
     up((void **)&h->boundary, bd.data(), bd.size() * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&h->sendbuf, std::max<int64_t>(so, 1) * sizeof(double));
-    if (e == cudaSuccess) e = cudaMalloc(&h->halo, std::max<int64_t>(ro, 1) * sizeof(double));
+    // p2p: two halo buffers (exchange parity) for the fused launch
+    h->fused = ctx->halo_p2p > 0 && ctx->p2p_fused &&
+               h->interior_runs.size() + h->boundary_runs.size() <= SELL_RUNS;
+    if (e == cudaSuccess)
+        e = cudaMalloc(&h->halo, std::max<int64_t>(ro, 1) * (ctx->halo_p2p > 0 ? 2 : 1) * sizeof(double));
     if (e != cudaSuccess) {
         halo_free(h);
         return amgp_cuda_fail(e, "halo plan upload", __FILE__, __LINE__);
@@ -455,15 +474,11 @@ __global__ void k_halo_signal(unsigned long long *sync, int nranks, int nrecvp,
     for (int i = 0; i < nrecvp; i++) st_release_sys(consumed_remote[i], e);
 }
 
-// inline: the pack runs on the compute stream ahead of a fused launch (whose
-// boundary CTAs spin, so the pack must never wait for SM slots behind them)
-static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x, bool inline_pack) {
+static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
     if (h.nsend == 0) return AMGP_OK;
-    cudaStream_t st = inline_pack ? ctx->stream : ctx->comm_stream;
-    if (!inline_pack) {
-        AMGP_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
-        AMGP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
-    }
+    cudaStream_t st = ctx->comm_stream;
+    AMGP_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
+    AMGP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
     // launched with the highest priority explicitly (kept when captured into
     // a graph): its CTAs must be scheduled ahead of the interior rows
     cudaLaunchConfig_t cfg = {};
@@ -480,12 +495,11 @@ static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x, bool inl
                                  h.sync_slot, ctx->nranks, (const int *)h.d_sendp, h.nsendp,
                                  (unsigned long long *const *)h.d_ready_remote));
     AMGP_CHECK_LAUNCH(ctx);
-    if (!inline_pack) AMGP_CUDA(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
+    AMGP_CUDA(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
     return AMGP_OK;
 }
 
-static int p2p_end(amgp_ctx *ctx, const HaloPlan &h, bool inline_pack) {
-    if (inline_pack) return AMGP_OK;
+static int p2p_end(amgp_ctx *ctx, const HaloPlan &h) {
     // the pack kernel must not be overtaken by the next exchange's; the
     // data itself is awaited inside the boundary kernels (halo_wait)
     if (h.nsend > 0) AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
@@ -501,10 +515,10 @@ int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A) {
     return AMGP_OK;
 }
 
-int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x, bool inline_pack) {
+int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
     const HaloPlan &h = *A->halo;
     if (ctx->halo_p2p < 0) return AMGP_OK;
-    if (ctx->halo_p2p) return p2p_begin(ctx, h, x, inline_pack);
+    if (ctx->halo_p2p) return p2p_begin(ctx, h, x);
     NcclApi *api = nccl();
     if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator for the halo exchange");
     if (h.nsend > 0) {
@@ -529,9 +543,9 @@ int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x, bool 
     return AMGP_OK;
 }
 
-int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A, bool inline_pack) {
+int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A) {
     if (ctx->halo_p2p < 0) return AMGP_OK;
-    if (ctx->halo_p2p) return p2p_end(ctx, *A->halo, inline_pack);
+    if (ctx->halo_p2p) return p2p_end(ctx, *A->halo);
     AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
     return AMGP_OK;
 }

@@ -410,6 +410,14 @@ int prolong_add_enqueue(amgp_ctx *ctx, const amgp_mat *P, const double *xc, doub
 // SpMV.  use_graph & 2: only the halo exchanges (transport latency).
 static int exchange_only(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
     if (!A->halo) return AMGP_OK;
+    if (A->halo->fused) {  // fused protocol: a launch of pack CTAs + one waiting CTA, no rows
+        SellView v = view_of(A);
+        fused_view(ctx, A, v);
+        v.nruns = 0;
+        v.nlist = 0;
+        v.nfirst = 0;
+        return launch_view(ctx, A, v, x, SpmvEpi<0>{nullptr, nullptr});
+    }
     AMGP_TRY(halo_exchange_begin(ctx, A, x));
     AMGP_TRY(halo_exchange_end(ctx, A));
     return halo_exchange_done(ctx, A);

@@ -19,6 +19,8 @@
 // so adding +0.0 leaves it unchanged bit for bit.
 #pragma once
 
+#include <algorithm>
+
 #include "amgp_common.cuh"
 
 #define ROWS_BLOCK 256
@@ -35,35 +37,55 @@
 // Launch modes.  ROWS_PLAIN: slices of the run table, every column local
 // (single-GPU matrices, interior slices of distributed ones).  ROWS_GEN: a
 // slice list and/or halo columns (boundary slices) -- kept out of the common
-// kernel so its gather stays one load per slot.  ROWS_FUSED (p2p transport):
-// interior AND boundary slices in one launch; launch indices < nfirst are
-// interior (plain gather, no wait), the rest wait for the halo in-kernel
-// (halo_wait, CTA-uniform) and gather through it; the last CTA to finish
-// completes the exchange (halo_complete).
+// kernel so its gather stays one load per slot.  ROWS_FUSED (p2p transport,
+// amgp_common.cuh "fused launch"): launch indices < npack pack the operand
+// into the neighbours' halo buffers; the rest are slices of the run table,
+// interior first (plain gather, no wait), then boundary (pack help, in-kernel
+// halo wait, gather through the parity buffer).  CTA-uniform branches.
 enum { ROWS_PLAIN = 0, ROWS_GEN = 1, ROWS_FUSED = 2 };
 
-template <class Epi, int MODE>
-__global__ void __launch_bounds__(ROWS_BLOCK)
-k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
-    const int64_t first = (int64_t)blockIdx.x * ROWS_SLICES;
-    const bool bnd = MODE == ROWS_FUSED && first + ROWS_SLICES > A.nfirst;  // CTA-uniform
-    if (MODE == ROWS_GEN || bnd) halo_wait(A);
-    const int64_t idx = first + (threadIdx.x >> 5);
+// Rows of launch CTA `cta` (ROWS_SLICES slices): y = A x (halo-aware gather
+// when HALO), then the epilogue.
+template <class Epi, int MODE, bool HALO>
+__device__ __forceinline__ void thread_rows_body(const SellView &A, int64_t cta,
+                                                 const double *__restrict__ xg,
+                                                 const double *__restrict__ xh, const Epi &epi) {
+    const int64_t idx = cta * ROWS_SLICES + (threadIdx.x >> 5);
     const int lane = threadIdx.x & 31;
-    if (idx < A.nlist) {
-        const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[idx] : run_slice(A, idx);
-        double y = 0.0;
-        if (Epi::kSpmv) {
-            if (MODE == ROWS_GEN || (MODE == ROWS_FUSED && idx >= A.nfirst))
-                y = sell_row_dot<ROWS_U, true>(A, s, lane, xg);
-            else
-                y = sell_row_dot<ROWS_U, false>(A, s, lane, xg);
+    if (idx >= A.nlist) return;
+    const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[idx] : run_slice(A, idx);
+    double y = 0.0;
+    if (Epi::kSpmv) y = sell_row_dot<ROWS_U, HALO>(A, s, lane, xg, xh);
+    const int64_t row = s * 32 + lane;
+    if (row < A.nrows) epi(row, y);
+}
+
+template <class Epi, int MODE>
+__global__ void __launch_bounds__(ROWS_BLOCK, 8)  // 32 registers: 8 CTAs per SM
+k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
+    if (MODE == ROWS_PLAIN) {
+        thread_rows_body<Epi, MODE, false>(A, blockIdx.x, xg, nullptr, epi);
+    } else if (MODE == ROWS_GEN) {
+        halo_wait(A);
+        thread_rows_body<Epi, MODE, true>(A, blockIdx.x, xg, A.xh, epi);
+        if (A.complete) halo_complete(A, gridDim.x);
+    } else {
+        // separate paths, so the interior rows keep the plain kernel's registers
+        const int64_t cta = (int64_t)blockIdx.x - A.npack;
+        if (cta < 0) {  // pack CTA
+            const unsigned long long e = fused_epoch(A);
+            fused_pack(A, e, xg);
+            fused_complete(A, e, (unsigned)A.ncounted);
+        } else if ((cta + 1) * ROWS_SLICES <= A.nfirst) {  // interior slices only
+            thread_rows_body<Epi, MODE, false>(A, cta, xg, nullptr, epi);
+        } else {  // boundary: help the pack, wait for the halo, gather through it
+            const unsigned long long e = fused_epoch(A);
+            fused_pack(A, e, xg);
+            fused_wait(A, e);
+            thread_rows_body<Epi, MODE, true>(A, cta, xg, A.xh + (int64_t)(e & 1ull) * A.xh_stride, epi);
+            fused_complete(A, e, (unsigned)A.ncounted);
         }
-        const int64_t row = s * 32 + lane;
-        if (row < A.nrows) epi(row, y);
     }
-    if (bnd) halo_complete(A, gridDim.x - (unsigned)(A.nfirst / ROWS_SLICES));
-    if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }
 
 // NW warps, U slot loads in flight per thread: SPLIT_WARPS x SPLIT_U for
@@ -74,9 +96,31 @@ template <class Epi, int MODE, int NW, int U>
 __global__ void __launch_bounds__(NW * 32)
 k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     __shared__ double prod[SPLIT_CHUNK * 32];
-    const bool halo = MODE == ROWS_GEN || (MODE == ROWS_FUSED && (int64_t)blockIdx.x >= A.nfirst);
-    if (halo) halo_wait(A);
-    const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[blockIdx.x] : run_slice(A, blockIdx.x);
+    int64_t cta = blockIdx.x;
+    unsigned long long e = 0;
+    if (MODE == ROWS_FUSED) {
+        if (cta < A.npack) {
+            e = fused_epoch(A);
+            fused_pack(A, e, xg);
+            fused_complete(A, e, (unsigned)A.ncounted);
+            return;
+        }
+        cta -= A.npack;
+    }
+    const bool halo = MODE == ROWS_GEN || (MODE == ROWS_FUSED && cta >= A.nfirst);
+    const double *xh = A.xh;
+    if (MODE == ROWS_GEN) halo_wait(A);
+    if (MODE == ROWS_FUSED && halo) {
+        e = fused_epoch(A);
+        fused_pack(A, e, xg);
+        fused_wait(A, e);
+        xh += (int64_t)(e & 1ull) * A.xh_stride;
+        if (cta >= A.nlist) {  // exchange-only launch: wait and complete, no rows
+            fused_complete(A, e, (unsigned)A.ncounted);
+            return;
+        }
+    }
+    const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[cta] : run_slice(A, cta);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
@@ -102,7 +146,7 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                     double p = 0.0;
                     if (cc[u] >= 0)
                         p = __dmul_rn(vv[u], ld_gather_f64(MODE != ROWS_PLAIN && halo && cc[u] >= A.nown
-                                                               ? A.xh + (cc[u] - A.nown)
+                                                               ? xh + (cc[u] - A.nown)
                                                                : xg + cc[u],
                                                            pl));
                     prod[jj * 32 + lane] = p;
@@ -120,7 +164,7 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
         const int64_t row = s * 32 + lane;
         if (row < A.nrows) epi(row, sum);
     }
-    if (MODE == ROWS_FUSED && halo) halo_complete(A, gridDim.x - (unsigned)A.nfirst);
+    if (MODE == ROWS_FUSED && halo) fused_complete(A, e, (unsigned)A.ncounted);
     if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }
 
@@ -130,24 +174,41 @@ inline bool use_split(const amgp_mat *A) {
     return A->max_width >= 24 && A->nslices < 148 * 64;
 }
 
+// pack CTAs of a fused launch with block size bs: one per chunk, <= 1 per SM
+inline int fused_npack(const SellView &v, int bs) {
+    const int64_t csize = (int64_t)(bs / 32) * FUSED_CHUNK;
+    return (int)std::min<int64_t>((v.nsend + csize - 1) / csize, 148);
+}
+
 template <class Epi, int MODE>
-void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v, const double *xg,
+void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const double *xg,
                  const Epi &epi) {
-    const unsigned gs = (unsigned)v.nlist, gt = grid_for(v.nlist, ROWS_SLICES);
-    if (Epi::kSpmv && use_split(A)) {
-        if (v.nlist < 2 * 148)
-            k_split_rows<Epi, MODE, 24, 8><<<gs, 24 * 32, 0, ctx->stream>>>(v, xg, epi);
+    SellView v = v0;
+    const bool split = Epi::kSpmv && use_split(A);
+    const int nw = v.nlist < 2 * 148 ? 24 : SPLIT_WARPS;
+    const int bs = split ? nw * 32 : ROWS_BLOCK;
+    unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);
+    if (MODE == ROWS_FUSED) {  // pack CTAs first; at least one CTA waits and completes
+        v.npack = fused_npack(v, bs);
+        const int64_t first_bnd = split ? v.nfirst : v.nfirst / ROWS_SLICES;  // first waiting CTA
+        const int64_t nrow_ctas = std::max<int64_t>(grid, first_bnd + 1);
+        v.ncounted = v.npack + (nrow_ctas - first_bnd);
+        grid = (unsigned)(v.npack + nrow_ctas);
+    }
+    if (split) {
+        if (nw == 24)
+            k_split_rows<Epi, MODE, 24, 8><<<grid, 24 * 32, 0, ctx->stream>>>(v, xg, epi);
         else
-            k_split_rows<Epi, MODE, SPLIT_WARPS, SPLIT_U><<<gs, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+            k_split_rows<Epi, MODE, SPLIT_WARPS, SPLIT_U><<<grid, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
     } else {
-        k_thread_rows<Epi, MODE><<<gt, ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
+        k_thread_rows<Epi, MODE><<<grid, ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
     }
 }
 
 template <class Epi>
 int launch_view(amgp_ctx *ctx, const amgp_mat *A, const SellView &v, const double *xg,
                 const Epi &epi) {
-    if (v.nlist == 0) return AMGP_OK;
+    if (v.nlist == 0 && !v.fused) return AMGP_OK;
     if (v.fused) launch_mode<Epi, ROWS_FUSED>(ctx, A, v, xg, epi);
     else if (v.slist || v.xh) launch_mode<Epi, ROWS_GEN>(ctx, A, v, xg, epi);
     else launch_mode<Epi, ROWS_PLAIN>(ctx, A, v, xg, epi);
@@ -155,12 +216,49 @@ int launch_view(amgp_ctx *ctx, const amgp_mat *A, const SellView &v, const doubl
     return AMGP_OK;
 }
 
+// Fill the fused-launch fields of a view of distributed matrix A (runs:
+// interior then boundary; HaloPlan::fused).
+inline void fused_view(amgp_ctx *ctx, const amgp_mat *A, SellView &v) {
+    const HaloPlan &h = *A->halo;
+    v.sync_slot = h.sync_slot;
+    v.recvp = h.d_recvp;
+    v.nrecvp = h.nrecvp;
+    v.nranks = ctx->nranks;
+    v.consumed_remote = h.d_consumed_remote;
+    v.slist = nullptr;
+    v.nruns = 0;
+    int64_t end = 0;
+    for (const auto *set : {&h.interior_runs, &h.boundary_runs})
+        for (const auto &r : *set) {
+            v.run_s0[v.nruns] = r.first;
+            end += r.second;
+            v.run_end[v.nruns++] = end;
+        }
+    v.nlist = end;
+    v.fused = 1;
+    v.nfirst = h.n_interior;
+    v.nown = h.nown;
+    v.xh = h.halo;
+    v.xh_stride = h.nhalo;
+    v.npeers = (int)h.peers.size();
+    v.nsend = h.nsend;
+    v.send_idx = h.send_idx;
+    v.seg = h.d_seg;
+    v.dest = h.d_dest;
+    v.sendp = h.d_sendp;
+    v.nsendp = h.nsendp;
+    v.ready_remote = h.d_ready_remote;
+    v.sym = h.sym;
+    v.ctr = AMGP_SYNC_CTR(ctx->nranks);
+}
+
 // y-rows of A with epilogue epi, gathering operand xg.  For a distributed
 // matrix the halo of xg travels while the interior slices (no halo column)
-// compute.  NCCL transport: interior launch, join the comm stream, boundary
-// launch.  p2p transport: one ROWS_FUSED launch when both slice sets are a
-// few runs (boundary CTAs wait for the halo in-kernel), else the same two
-// launches with in-kernel waits and a completion kernel.
+// compute: interior launch, exchange (NCCL on the comm stream, or the p2p
+// pack kernel on the high-priority stream), boundary launch (p2p: in-kernel
+// waits; it completes the exchange).  AMGP_P2P_FUSED=1 (HaloPlan::fused):
+// ONE ROWS_FUSED launch (pack CTAs, interior slices, boundary slices that
+// wait for the halo in-kernel) when the slice sets are a few runs.
 template <class Epi>
 int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &epi) {
     if (!Epi::kSpmv || !A->halo) {
@@ -170,11 +268,12 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     const HaloPlan &h = *A->halo;
     const bool p2p = ctx->halo_p2p > 0;
     if (A->nslices == 0 && !p2p) return AMGP_OK;
-    // (the fused launch's boundary CTAs complete the exchange: needs >= 1)
-    const bool fused = p2p && ctx->p2p_fused && h.n_boundary > 0 &&
-                       h.interior_runs.size() + h.boundary_runs.size() <= SELL_RUNS;
-    AMGP_TRY(halo_exchange_begin(ctx, A, xg, fused));
     SellView v = view_of(A);
+    if (h.fused) {
+        fused_view(ctx, A, v);
+        return launch_view(ctx, A, v, xg, epi);
+    }
+    AMGP_TRY(halo_exchange_begin(ctx, A, xg));
     if (p2p) {
         v.sync_slot = h.sync_slot;
         v.recvp = h.d_recvp;
@@ -193,16 +292,6 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
         }
         v.nlist = end;
     };
-    if (fused) {
-        std::vector<std::pair<int64_t, int64_t>> runs(h.interior_runs);
-        runs.insert(runs.end(), h.boundary_runs.begin(), h.boundary_runs.end());
-        set_runs(runs);
-        v.fused = 1;
-        v.nfirst = h.n_interior;
-        v.nown = h.nown;
-        v.xh = h.halo;
-        return launch_view(ctx, A, v, xg, epi);
-    }
     // a set of at most SELL_RUNS contiguous runs is one launch over the run
     // table (no slice-list indirection), else one launch over the list
     auto launch_set = [&](const std::vector<std::pair<int64_t, int64_t>> &runs,

@@ -234,14 +234,20 @@ class _SharedArrays:
         return os.path.exists(os.path.join(self.path, key + ".npy"))
 
 
-def share_hierarchy(h_or_builder, comm_rank, barrier):
+def share_hierarchy(h_or_builder, comm_rank, barrier, cache=None):
     """Rank 0 builds (callable) or holds the host hierarchy and writes its
     arrays as .npy files to /dev/shm (or the temp dir when /dev/shm is too
-    small); every rank memory-maps them.  Returns (arrays, directory)."""
+    small); every rank memory-maps them.  Returns (arrays, directory).
+    cache: a directory kept across runs -- reused when it holds a complete
+    hierarchy (e.g. one setup for a strong-scaling sweep over world sizes),
+    else written there; the caller does not release it."""
     import shutil
 
     name = f"amgp_hier_{os.environ.get('MASTER_PORT', '0')}"
     where = os.path.join(tempfile.gettempdir(), name + ".where")
+    if cache is not None and os.path.exists(os.path.join(cache, "complete")):
+        barrier()
+        return _SharedArrays(cache), cache
     if comm_rank == 0:
         h = h_or_builder() if callable(h_or_builder) else h_or_builder
         need = 2 * sum(lv.A.nnz * 16 + (lv.P.nnz * 32 if lv.P is not None else 0) for lv in h.levels)
@@ -250,7 +256,7 @@ def share_hierarchy(h_or_builder, comm_rank, barrier):
             base = tempfile.gettempdir()
             if os.path.isdir("/dev/shm") and shutil.disk_usage("/dev/shm").free > need:
                 base = "/dev/shm"
-        path = os.path.join(base, name)
+        path = cache if cache is not None else os.path.join(base, name)
         shutil.rmtree(path, ignore_errors=True)
         os.makedirs(path)
         arrs = {"nlev": np.array([len(h.levels)]), "coarse_sweeps": np.array([h.coarse_sweeps])}
@@ -263,6 +269,7 @@ def share_hierarchy(h_or_builder, comm_rank, barrier):
             arrs[f"M{l}"] = np.asarray(lv.M.m_diag)
         for k, a in arrs.items():
             np.save(os.path.join(path, k + ".npy"), a)
+        open(os.path.join(path, "complete"), "w").close()
         with open(where, "w") as f:
             f.write(path)
     barrier()

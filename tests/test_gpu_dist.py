@@ -50,7 +50,7 @@ def test_dist_check_two_gpus(graph, transport):
     env = dict(os.environ)
     env.pop("AMGP_P2P_FUSED", None)
     env["AMGP_HALO"] = "nccl" if transport == "nccl" else "p2p"
-    if transport == "p2p_fused":
+    if transport == "p2p_fused":  # one launch: pack CTAs + interior + boundary (halo double-buffered)
         env["AMGP_P2P_FUSED"] = "1"
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]

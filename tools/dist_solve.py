@@ -3,6 +3,7 @@
 
     torchrun --nproc-per-node 2 --master-addr 127.0.0.1 tools/dist_solve.py \
         --grid 161 --replicate-below 20000 50000 200000 --graph 0 1
+    (--stencil 27 --family opt_cheb1 --k 3: BASELINE configs[4] shape)
 """
 
 import argparse
@@ -18,11 +19,13 @@ sys.path.insert(0, REPO)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=161)
+    ap.add_argument("--stencil", type=int, default=7, choices=[7, 27])
     ap.add_argument("--family", default="opt_cheb4")
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--replicate-below", type=int, nargs="+", default=[20000])
     ap.add_argument("--graph", type=int, nargs="+", default=[1])
     ap.add_argument("--repeat", type=int, default=3)
+    ap.add_argument("--cache", default=None, help="hierarchy directory kept across runs (strong scaling)")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -37,11 +40,11 @@ def main():
     cfg = P.PolySmootherConfig(family=args.family, degree=args.k)
 
     def build():
-        A, _ = P.poisson3d(args.grid)
+        A, _ = (P.poisson3d if args.stencil == 7 else P.poisson3d_27)(args.grid)
         return P.build_hierarchy(A, smoother=cfg)
 
     t0 = time.perf_counter()
-    d, path = D.share_hierarchy(build, comm.rank, dist.barrier)
+    d, path = D.share_hierarchy(build, comm.rank, dist.barrier, cache=args.cache)
     setup = time.perf_counter() - t0
     res = []
     for rb in args.replicate_below:
@@ -61,9 +64,13 @@ def main():
                         "solve_ms": [round(1e3 * t, 3) for t in times]})
             del dh
     if comm.rank == 0:
-        print(json.dumps({"grid": args.grid, "world": comm.size, "setup_s": setup, "runs": res}),
+        print(json.dumps({"grid": args.grid, "stencil": args.stencil, "family": args.family, "k": args.k,
+                          "world": comm.size, "setup_s": setup,
+                          "levels": [int(d[f"A{l}_shape"][0]) for l in range(int(d["nlev"][0]))],
+                          "runs": res}),
               flush=True)
-        D.release_shared(path)
+        if args.cache is None:
+            D.release_shared(path)
     dist.barrier()
     dist.destroy_process_group()
 

@@ -243,10 +243,13 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
 // halo of the current exchange (epoch + 1) has arrived from every sender.
 __device__ __forceinline__ void halo_wait(const SellView &A) {
     if (A.nrecvp == 0) return;
-    if (threadIdx.x == 0) {
-        const unsigned long long e = ld_acquire_sys(A.sync_slot + 2 * A.nranks) + 1;
-        for (int i = 0; i < A.nrecvp; i++)
-            while (ld_acquire_sys(A.sync_slot + A.recvp[i]) < e) __nanosleep(20);
+    if (threadIdx.x == 0) {  // relaxed polls, one acquire (an acquire load invalidates the SM's L1)
+        const unsigned long long e = ld_relaxed_gpu(A.sync_slot + 2 * A.nranks) + 1;
+        for (int i = 0; i < A.nrecvp; i++) {
+            const unsigned long long *w = A.sync_slot + A.recvp[i];
+            while (ld_relaxed_sys(w) < e) __nanosleep(20);
+            (void)ld_acquire_sys(w);
+        }
     }
     __syncthreads();
 }

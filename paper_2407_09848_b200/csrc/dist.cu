@@ -440,10 +440,13 @@ __global__ void k_pack_p2p(int64_t n, int npeers, const int64_t *__restrict__ id
                            const int *__restrict__ sendp, int nsendp,
                            unsigned long long *const *__restrict__ ready_remote) {
     __shared__ unsigned long long epoch;
-    if (threadIdx.x == 0) {
-        epoch = ld_acquire_sys(sync + 2 * nranks);
-        for (int i = 0; i < nsendp; i++)
-            while (ld_acquire_sys(sync + nranks + sendp[i]) < epoch) __nanosleep(20);
+    if (threadIdx.x == 0) {  // relaxed polls, one acquire (an acquire load invalidates the SM's L1)
+        epoch = ld_relaxed_gpu(sync + 2 * nranks);
+        for (int i = 0; i < nsendp; i++) {
+            const unsigned long long *w = sync + nranks + sendp[i];
+            while (ld_relaxed_sys(w) < epoch) __nanosleep(20);
+            (void)ld_acquire_sys(w);
+        }
     }
     __syncthreads();
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;

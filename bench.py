@@ -240,17 +240,18 @@ def cpu_baseline(m):
                       f"({tot_t:.1f} s)"}
 
 
-def solve_bench(m, kind="smoothed_aggregation", cpu=True):
-    """PCG + AMG V-cycle solve (BASELINE metric part 2) on poisson3d(m):
-    native host setup, then per smoother family (k=4) one device solve at
-    rtol 1e-6 timed with CUDA events on the library stream; the C oracle
-    solves the same hierarchy on the host for the CPU column."""
+def solve_bench(m, kind="smoothed_aggregation", cpu=True, stencil=7, k=4, cpu_family="opt_cheb1"):
+    """PCG + AMG V-cycle solve (BASELINE metric part 2) on poisson3d(m)
+    (7-point) or the 27-point stencil: native host setup, then per smoother
+    family (degree k) one device solve at rtol 1e-6 timed with CUDA events on
+    the library stream; the C oracle solves the same hierarchy on the host
+    (all cores) for the CPU column."""
     import torch
 
     import paper_2407_09848_b200 as P
     from paper_2407_09848_b200 import _native as N
 
-    A, b = P.poisson3d(m)
+    A, b = (P.poisson3d if stencil == 7 else P.poisson3d_27)(m)
     t0 = time.perf_counter()
     h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
                           smoother=P.PolySmootherConfig(family="opt_cheb1", degree=4))
@@ -261,11 +262,12 @@ def solve_bench(m, kind="smoothed_aggregation", cpu=True):
     c = D.ctx
     bd = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
     cfg_k = P.KrylovConfig(tol=1e-6, itmax=1000)
-    out = {"m": m, "n": A.nrows, "coarsening": kind, "levels": [lv.A.nrows for lv in h.levels],
+    out = {"m": m, "n": A.nrows, "stencil": stencil, "degree": k, "coarsening": kind,
+           "levels": [lv.A.nrows for lv in h.levels],
            "operator_complexity": h.operator_complexity(), "setup_s": setup_s,
            "upload_s": upload_s, "tol": 1e-6, "results": {}}
     for fam in ("opt_cheb1", "cheb4", "opt_cheb4", "l1_jacobi"):
-        cfg = P.PolySmootherConfig(family=fam, degree=4)
+        cfg = P.PolySmootherConfig(family=fam, degree=k)
         for lv in h.levels:
             lv.smoother = cfg
         pre = P.as_vcycle_preconditioner(h)
@@ -286,22 +288,24 @@ def solve_bench(m, kind="smoothed_aggregation", cpu=True):
                **({"P": (l.P.row_ptr, l.P.col_idx, l.P.values),
                    "R": (l.restrict_op().row_ptr, l.restrict_op().col_idx, l.restrict_op().values)}
                   if l.P is not None else {})} for l in h.levels]
-        cfg = P.PolySmootherConfig(family="opt_cheb1", degree=4)
-        oh = oracle.Hierarchy(lv, "opt_cheb1", 4, a=cfg.a)
+        cfg = P.PolySmootherConfig(family=cpu_family, degree=k)
+        beta = cfg.beta.beta if cfg.family == "opt_cheb4" else None
+        oh = oracle.Hierarchy(lv, cpu_family, k, a=cfg.a or 0.0, beta=beta)
         threads = oracle.max_threads()
         oracle.set_threads(threads)
         t0 = time.perf_counter()
         _, it, rr, conv, brk, _ = oracle.pcg(lv[0]["A"], np.ones(A.nrows), oh, tol=1e-6)
-        out["cpu_opt_cheb1"] = {"iterations": it, "final_relres": rr,
+        out["cpu_" + cpu_family] = {"iterations": it, "final_relres": rr,
                                 "solve_s": time.perf_counter() - t0, "cores": threads,
                                 "kind": "port"}
         oracle.set_threads(1)
     return out
 
 
-def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4):
-    """Weak-scaled PCG + AMG solve over all ranks (BASELINE configs[3] shape):
-    global cube round(m_base N^(1/3)), hierarchy built once on rank 0 (native
+def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, strong=False):
+    """PCG + AMG solve over all ranks: weak-scaled (BASELINE configs[3]
+    shape: global cube round(m_base N^(1/3))) or strong-scaled (configs[4]
+    shape: global cube m_base), hierarchy built once on rank 0 (native
     setup) and shared, every level row-partitioned (coarse levels
     replicated).  Returns (on every rank) iterations and max-over-ranks time."""
     import torch
@@ -310,12 +314,12 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4):
     import paper_2407_09848_b200 as P
     from paper_2407_09848_b200 import dist as Dist
 
-    m = int(round(m_base * ws ** (1.0 / 3.0)))
+    m = m_base if strong else int(round(m_base * ws ** (1.0 / 3.0)))
     cfg = P.PolySmootherConfig(family=family, degree=k)
     t0 = time.perf_counter()
 
     def build():
-        A, _ = P.poisson3d(m)
+        A, _ = (P.poisson3d if stencil == 7 else P.poisson3d_27)(m)
         return P.build_hierarchy(A, smoother=cfg)
 
     d, path = Dist.share_hierarchy(build, comm.rank, dist.barrier)
@@ -341,7 +345,8 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4):
             Dist.release_shared(path)
         except OSError:
             pass
-    return {"m": m, "n": int(m ** 3), "rows_per_gpu": hi - lo, "family": family, "degree": k,
+    return {"m": m, "n": int(m ** 3), "stencil": stencil, "scaling": "strong" if strong else "weak",
+            "rows_per_gpu": hi - lo, "family": family, "degree": k,
             "levels": [int(d[f"A{l}_shape"][0]) for l in range(int(d["nlev"][0]))],
             "distributed_levels": sum(p is not None for p in dh.parts),
             "setup_s": setup_s, "iterations": rep.iterations, "final_relres": rep.final_relres,
@@ -463,7 +468,9 @@ def run_b200(args):
 
     dsolve = None
     if ws > 1 and args.solve_grid > 0:
-        dsolve = dist_solve_bench(comm, args.solve_grid, ws)
+        dsolve = dist_solve_bench(comm, args.solve_grid, ws, family=args.solve_family or "opt_cheb4",
+                                  k=args.solve_k, stencil=args.solve_stencil,
+                                  strong=args.solve_scaling == "strong")
 
     if rank == 0:
         line = {
@@ -494,7 +501,9 @@ def run_b200(args):
         if ws == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_baseline(args.cpu_grid)
         if ws == 1 and args.solve_grid > 0:
-            line["solve"] = solve_bench(args.solve_grid, cpu=not args.no_cpu_baseline)
+            line["solve"] = solve_bench(args.solve_grid, cpu=not args.no_cpu_baseline,
+                                        stencil=args.solve_stencil, k=args.solve_k,
+                                        cpu_family=args.solve_family or "opt_cheb1")
         if dsolve is not None:
             line["solve"] = dsolve
         print(json.dumps(line), flush=True)
@@ -516,6 +525,13 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--solve-grid", type=int, default=128,
                     help="grid size of the PCG+AMG solve section (0: skip)")
+    ap.add_argument("--solve-stencil", type=int, default=7, choices=[7, 27])
+    ap.add_argument("--solve-k", type=int, default=4, help="smoother degree of the solve section")
+    ap.add_argument("--solve-family", default=None,
+                    help="smoother family of the multi-GPU solve / the CPU oracle solve "
+                         "(default opt_cheb4 / opt_cheb1)")
+    ap.add_argument("--solve-scaling", default="weak", choices=["weak", "strong"],
+                    help="N > 1: weak (solve-grid^3 rows per GPU) or strong (solve-grid^3 in total)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3

@@ -284,6 +284,10 @@ Cmp canonical(const Cmp &A) {
         });
 }
 
+// Free an intermediate as soon as its last consumer is done (the setup's
+// host-memory peak is the fine level's Galerkin product: n rows of A P).
+void release(Cmp &m) { Cmp().p.swap(m.p), Cmp().i.swap(m.i), Cmp().x.swap(m.x); }
+
 Cmp from_host(int64_t nrows, int64_t ncols, const int64_t *rp, const int64_t *ci, const double *v) {
     Cmp A;
     A.nmajor = nrows;
@@ -517,9 +521,13 @@ int amgp_setup_smooth_prolongator(int64_t n, const int64_t *rp, const int64_t *c
             }
             return c;
         });
+    release(A);
     Cmp Ph = prolongator(n, agg, n_agg);
     Cmp T = matmat(S, Ph);
+    release(S);
     Cmp R = binop(Ph, T, [](double a, double b) { return a - b; });
+    release(T);
+    release(Ph);
     *out = wrap(canonical(R));
     return AMGP_OK;
 }
@@ -529,17 +537,31 @@ int amgp_setup_galerkin(int64_t n, const int64_t *rp, const int64_t *ci, const d
                         int64_t nc, const int64_t *prp, const int64_t *pci, const double *pv,
                         amgp_hcsr **out) {
     if (n < 0 || !rp || !prp || !out) return amgp_fail(AMGP_EINVAL, "galerkin: bad argument");
-    Cmp A = from_host(n, n, rp, ci, v);
+    Cmp At;
+    {
+        Cmp A = from_host(n, n, rp, ci, v);
+        At = compress_t(A);
+    }
     Cmp P = from_host(n, nc, prp, pci, pv);
-    Cmp C = matmat(compress_t(A), P);  // P^T (CSC) @ A: csr_matmat(csc(A), P)
-    Cmp G = matmat(compress_t(P), C);  // C (CSC) @ P:  csr_matmat(csc(P), C)
+    Cmp C = matmat(At, P);  // P^T (CSC) @ A: csr_matmat(csc(A), P)
+    release(At);
+    Cmp G;
+    {
+        Cmp Pt = compress_t(P);
+        release(P);
+        G = matmat(Pt, C);  // C (CSC) @ P:  csr_matmat(csc(P), C)
+    }
+    release(C);
     // G holds "column J -> rows K" of P^T A P.  S = G + G^T evaluated as CSC:
     // the CSR view G^T converted to CSC is compress_t(G arrays).
     Cmp H = compress_t(G);
     Cmp S = binop(G, H, [](double a, double b) { return a + b; });
+    release(G);
+    release(H);
     for (double &x : S.x) x = x * 0.5;
     // S is CSC (column t -> rows u); tocsr() == compressed transpose
     Cmp Sr = compress_t(S);
+    release(S);
     *out = wrap(canonical(Sr));
     return AMGP_OK;
 }

@@ -16,6 +16,7 @@ sys.path.insert(0, REPO)
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--m", type=int, default=64)
+    ap.add_argument("--stencil", type=int, default=7, choices=[7, 27])
     ap.add_argument("--kind", default="smoothed_aggregation")
     ap.add_argument("--family", default="opt_cheb1")
     ap.add_argument("--k", type=int, default=4)
@@ -28,7 +29,7 @@ def main():
     import paper_2407_09848_b200 as P
     from paper_2407_09848_b200 import _native as N
 
-    A, b = P.poisson3d(args.m)
+    A, b = (P.poisson3d if args.stencil == 7 else P.poisson3d_27)(args.m)
     t0 = time.perf_counter()
     h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=args.kind),
                           smoother=P.PolySmootherConfig(family=args.family, degree=args.k))
@@ -42,7 +43,7 @@ def main():
     for i in range(args.repeat):
         x, rep = P.solve(A, bd, precond=P.as_vcycle_preconditioner(h), cfg=P.KrylovConfig(tol=1e-6))
         torch.cuda.synchronize()
-        print(f"m={args.m} {args.kind} {args.family} k={args.k}: setup {setup:.2f}s "
+        print(f"m={args.m} {args.stencil}-pt {args.kind} {args.family} k={args.k}: setup {setup:.2f}s "
               f"iters {rep.iterations} relres {rep.final_relres:.3e} solve {rep.elapsed_s * 1e3:.2f} ms "
               f"levels {[lv.A.nrows for lv in h.levels]} tail_start {D.tail_start()}", flush=True)
 

@@ -24,6 +24,8 @@ def main():
     ap.add_argument("--grid", type=int, default=161)
     ap.add_argument("--reps", type=int, default=50)
     ap.add_argument("--replicate-below", type=int, default=20000)
+    ap.add_argument("--stencil", type=int, default=7, choices=[7, 27])
+    ap.add_argument("--cache", default=None, help="hierarchy directory kept across runs")
     args = ap.parse_args()
     import torch
     import torch.distributed as dist
@@ -41,10 +43,10 @@ def main():
     cfg = P.PolySmootherConfig(family="opt_cheb4", degree=4)
 
     def build():
-        A, _ = P.poisson3d(args.grid)
+        A, _ = (P.poisson3d if args.stencil == 7 else P.poisson3d_27)(args.grid)
         return P.build_hierarchy(A, smoother=cfg)
 
-    d, path = D.share_hierarchy(build, comm.rank, dist.barrier)
+    d, path = D.share_hierarchy(build, comm.rank, dist.barrier, cache=args.cache)
     L = int(d["nlev"][0])
     A_glob = [D._mat(d, f"A{l}") for l in range(L)]
 
@@ -96,10 +98,20 @@ def main():
                    "us_halo_graph": graph_us(Dh), "us_local_graph": graph_us(Dn),
                    "us_exchange_graph": graph_us(Dh, 3)}
             rows.append(rec)
+    # every rank's numbers; report the slowest rank (interior ranks have two
+    # neighbours) per matrix
+    allrows = [None] * comm.size
+    dist.all_gather_object(allrows, rows)
     if comm.rank == 0:
-        for r in rows:
-            print(json.dumps(r), flush=True)
-        D.release_shared(path)
+        for i, r in enumerate(rows):
+            per = [a[i] for a in allrows]
+            worst = max(per, key=lambda q: q["us_halo_graph"])
+            out = dict(worst)
+            out["rank_of_max"] = per.index(worst)
+            out["us_halo_graph_per_rank"] = [q["us_halo_graph"] for q in per]
+            print(json.dumps(out), flush=True)
+        if args.cache is None:
+            D.release_shared(path)
     dist.barrier()
     dist.destroy_process_group()
 

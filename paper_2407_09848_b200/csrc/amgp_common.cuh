@@ -241,17 +241,22 @@ __device__ __forceinline__ void st_release_sys(unsigned long long *p, unsigned l
 
 // Boundary kernels of the p2p transport: one thread per CTA waits until the
 // halo of the current exchange (epoch + 1) has arrived from every sender.
-__device__ __forceinline__ void halo_wait(const SellView &A) {
-    if (A.nrecvp == 0) return;
+// Returns the halo buffer of this exchange: the p2p halo is double-buffered
+// by exchange parity (xh_stride = nhalo; 0 for NCCL).  Every thread reads
+// the epoch itself: it only advances after every CTA of the launch has
+// passed the completion ticket (halo_complete).
+__device__ __forceinline__ const double *halo_wait(const SellView &A) {
+    if (A.nrecvp == 0) return A.xh;
+    const unsigned long long e = ld_relaxed_gpu(A.sync_slot + 2 * A.nranks);
     if (threadIdx.x == 0) {  // relaxed polls, one acquire (an acquire load invalidates the SM's L1)
-        const unsigned long long e = ld_relaxed_gpu(A.sync_slot + 2 * A.nranks) + 1;
         for (int i = 0; i < A.nrecvp; i++) {
             const unsigned long long *w = A.sync_slot + A.recvp[i];
-            while (ld_relaxed_sys(w) < e) __nanosleep(20);
+            while (ld_relaxed_sys(w) < e + 1) __nanosleep(20);
             (void)ld_acquire_sys(w);
         }
     }
     __syncthreads();
+    return A.xh + (int64_t)(e & 1ull) * A.xh_stride;
 }
 
 // End of a fused p2p launch, called by the nctas CTAs that waited for the
@@ -399,6 +404,7 @@ __device__ __forceinline__ void fused_complete(const SellView &A, unsigned long 
 int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x);
 int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A);
 int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A);  // after the boundary rows
+int halo_exchange_wait_done(amgp_ctx *ctx, const amgp_mat *A);  // exchange-only: wait, then complete
 void mat_free_halo(amgp_mat *A);
 void ctx_free_comm(amgp_ctx *ctx);  // communicator resources (amgp_ctx_destroy)
 int refresh_slice_maxcol(amgp_mat *A);  // recompute A->slice_maxcol from the device columns
@@ -493,10 +499,14 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
         }
 #pragma unroll
         for (int u = 0; u < U; u++) {
-            if (HALO)
-                xx[u] = cc[u] < 0 ? 0.0
-                                  : ld_gather_f64(cc[u] < A.nown ? x + cc[u] : xh + (cc[u] - A.nown), pl);
-            else
+            if (HALO) {
+                // branch-free operand select (own vector or halo buffer), so
+                // the U gathers stay one predicated batch
+                const int64_t c = cc[u];
+                const bool own = c < A.nown;
+                const double *p = (own ? x : xh) + (own ? c : c - A.nown);
+                xx[u] = cc[u] < 0 ? 0.0 : ld_gather_f64(p, pl);
+            } else
                 xx[u] = cc[u] < 0 ? 0.0 : ld_gather_f64(x + cc[u], pl);
         }
 #pragma unroll

@@ -27,9 +27,12 @@
 // IPC mapping, NVLink stores) and the kernels hand over ownership through
 // monotonic u64 epoch words (amgp_ctx::sync, one slot per distributed
 // matrix, peer-mapped):
-//   pack (comm stream)  waits consumed[dst] >= epoch (dst finished reading the
-//                       previous exchange), stores, and its last CTA sets
-//                       ready[me] = epoch + 1 on every receiver (release.sys)
+//   pack (comm stream)  stores into the receiver's halo buffer of parity
+//                       epoch & 1 (double-buffered), after consumed[dst] >=
+//                       epoch - 1 (dst finished reading exchange epoch - 2;
+//                       implied for symmetric exchanges, see k_pack_p2p), and
+//                       its last CTA sets ready[me] = epoch + 1 on every
+//                       receiver (release.sys)
 //   boundary rows       wait ready[src] >= epoch + 1 (acquire.sys) first
 //   completion          epoch += 1 and consumed[me] = epoch on every sender:
 //                       the boundary launch's last CTA, else k_halo_signal
@@ -431,29 +434,35 @@ __global__ void k_pack(int64_t n, const int64_t *__restrict__ idx, const double 
         out[i] = x[idx[i]];
 }
 
-// p2p pack: entry i of the send list goes straight to its receiver's halo.
-// Thread 0 of every CTA first waits until each receiver has consumed the
-// previous exchange; the last CTA to finish publishes the new epoch.
+// p2p pack: entry i of the send list goes straight to its receiver's halo
+// buffer of this exchange's parity (double-buffered: exchange e writes
+// buffer e & 1, so it only has to wait until each receiver has consumed
+// exchange e - 2 -- and not at all when every receiver also sends to me: my
+// launches of exchange e - 1 waited for its pack of e - 1, which its stream
+// issued after its boundary launch of e - 2).  The last CTA to finish
+// publishes the new epoch.
 __global__ void k_pack_p2p(int64_t n, int npeers, const int64_t *__restrict__ idx,
                            const double *__restrict__ x, double *const *__restrict__ dest,
                            const int64_t *__restrict__ seg, unsigned long long *sync, int nranks,
-                           const int *__restrict__ sendp, int nsendp,
+                           const int *__restrict__ sendp, int nsendp, int sym,
                            unsigned long long *const *__restrict__ ready_remote) {
-    __shared__ unsigned long long epoch;
-    if (threadIdx.x == 0) {  // relaxed polls, one acquire (an acquire load invalidates the SM's L1)
-        epoch = ld_relaxed_gpu(sync + 2 * nranks);
-        for (int i = 0; i < nsendp; i++) {
-            const unsigned long long *w = sync + nranks + sendp[i];
-            while (ld_relaxed_sys(w) < epoch) __nanosleep(20);
-            (void)ld_acquire_sys(w);
+    const unsigned long long epoch = ld_relaxed_gpu(sync + 2 * nranks);
+    if (!sym && epoch >= 2) {
+        if (threadIdx.x == 0) {  // relaxed polls, one acquire (an acquire load invalidates the SM's L1)
+            for (int i = 0; i < nsendp; i++) {
+                const unsigned long long *w = sync + nranks + sendp[i];
+                while (ld_relaxed_sys(w) + 1 < epoch) __nanosleep(20);
+                (void)ld_acquire_sys(w);
+            }
         }
+        __syncthreads();
     }
-    __syncthreads();
+    const int par = (int)(epoch & 1ull);
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * blockDim.x) {
         int q = 0;
         while (q + 1 < npeers && i >= seg[q + 1]) q++;
-        dest[q][i - seg[q]] = x[idx[i]];
+        dest[par * npeers + q][i - seg[q]] = x[idx[i]];
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -477,6 +486,30 @@ __global__ void k_halo_signal(unsigned long long *sync, int nranks, int nrecvp,
     for (int i = 0; i < nrecvp; i++) st_release_sys(consumed_remote[i], e);
 }
 
+// exchange-only diagnostic: wait for this exchange's halo, then complete it
+__global__ void k_halo_wait_signal(unsigned long long *sync, int nranks, const int *__restrict__ recvp,
+                                   int nrecvp, unsigned long long *const *__restrict__ consumed_remote) {
+    if (threadIdx.x != 0) return;
+    const unsigned long long e = sync[2 * nranks] + 1;
+    for (int i = 0; i < nrecvp; i++) {
+        while (ld_relaxed_sys(sync + recvp[i]) < e) __nanosleep(20);
+        (void)ld_acquire_sys(sync + recvp[i]);
+    }
+    sync[2 * nranks] = e;
+    __threadfence_system();
+    for (int i = 0; i < nrecvp; i++) st_release_sys(consumed_remote[i], e);
+}
+
+int halo_exchange_wait_done(amgp_ctx *ctx, const amgp_mat *A) {
+    if (ctx->halo_p2p <= 0) return AMGP_OK;
+    const HaloPlan &h = *A->halo;
+    if (h.peers.empty()) return AMGP_OK;
+    k_halo_wait_signal<<<1, 32, 0, ctx->stream>>>(h.sync_slot, ctx->nranks, h.d_recvp, h.nrecvp,
+                                                  h.d_consumed_remote);
+    AMGP_CHECK_LAUNCH(ctx);
+    return AMGP_OK;
+}
+
 static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
     if (h.nsend == 0) return AMGP_OK;
     cudaStream_t st = ctx->comm_stream;
@@ -495,7 +528,7 @@ static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
     cfg.numAttrs = 1;
     AMGP_CUDA(cudaLaunchKernelEx(&cfg, k_pack_p2p, h.nsend, (int)h.peers.size(), (const int64_t *)h.send_idx,
                                  (const double *)x, (double *const *)h.d_dest, (const int64_t *)h.d_seg,
-                                 h.sync_slot, ctx->nranks, (const int *)h.d_sendp, h.nsendp,
+                                 h.sync_slot, ctx->nranks, (const int *)h.d_sendp, h.nsendp, (int)h.sym,
                                  (unsigned long long *const *)h.d_ready_remote));
     AMGP_CHECK_LAUNCH(ctx);
     AMGP_CUDA(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));

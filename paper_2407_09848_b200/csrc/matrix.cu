@@ -420,7 +420,7 @@ static int exchange_only(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
     }
     AMGP_TRY(halo_exchange_begin(ctx, A, x));
     AMGP_TRY(halo_exchange_end(ctx, A));
-    return halo_exchange_done(ctx, A);
+    return ctx->halo_p2p > 0 ? halo_exchange_wait_done(ctx, A) : halo_exchange_done(ctx, A);
 }
 
 extern "C" int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y,

@@ -66,8 +66,8 @@ k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     if (MODE == ROWS_PLAIN) {
         thread_rows_body<Epi, MODE, false>(A, blockIdx.x, xg, nullptr, epi);
     } else if (MODE == ROWS_GEN) {
-        halo_wait(A);
-        thread_rows_body<Epi, MODE, true>(A, blockIdx.x, xg, A.xh, epi);
+        const double *xh = halo_wait(A);
+        thread_rows_body<Epi, MODE, true>(A, blockIdx.x, xg, xh, epi);
         if (A.complete) halo_complete(A, gridDim.x);
     } else {
         // separate paths, so the interior rows keep the plain kernel's registers
@@ -109,7 +109,7 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     }
     const bool halo = MODE == ROWS_GEN || (MODE == ROWS_FUSED && cta >= A.nfirst);
     const double *xh = A.xh;
-    if (MODE == ROWS_GEN) halo_wait(A);
+    if (MODE == ROWS_GEN) xh = halo_wait(A);
     if (MODE == ROWS_FUSED && halo) {
         e = fused_epoch(A);
         fused_pack(A, e, xg);
@@ -144,11 +144,11 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                 const int jj = j + u * NW;
                 if (jj < jn) {
                     double p = 0.0;
-                    if (cc[u] >= 0)
-                        p = __dmul_rn(vv[u], ld_gather_f64(MODE != ROWS_PLAIN && halo && cc[u] >= A.nown
-                                                               ? xh + (cc[u] - A.nown)
-                                                               : xg + cc[u],
-                                                           pl));
+                    // branch-free operand select (own vector or halo buffer)
+                    const int64_t c = cc[u];
+                    const bool hc = MODE != ROWS_PLAIN && halo && c >= A.nown;
+                    const double *src = (hc ? xh : xg) + (hc ? c - A.nown : c);
+                    if (cc[u] >= 0) p = __dmul_rn(vv[u], ld_gather_f64(src, pl));
                     prod[jj * 32 + lane] = p;
                 }
             }
@@ -168,10 +168,12 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }
 
-// Schedule choice: split when rows are long and there are too few slices to
-// keep the GPU's warps busy with thread-per-row.
-inline bool use_split(const amgp_mat *A) {
-    return A->max_width >= 24 && A->nslices < 148 * 64;
+// Schedule choice, per launch: split when rows are long and the launch has
+// too few slices to keep the GPU's warps busy with thread-per-row (e.g. the
+// boundary-slice launch of a distributed coarse level: ~800 slices of ~50
+// slots, latency bound at one thread per row).
+inline bool use_split(const amgp_mat *A, int64_t nslices_launched) {
+    return A->max_width >= 24 && nslices_launched < 148 * 64;
 }
 
 // pack CTAs of a fused launch with block size bs: one per chunk, <= 1 per SM
@@ -184,7 +186,7 @@ template <class Epi, int MODE>
 void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const double *xg,
                  const Epi &epi) {
     SellView v = v0;
-    const bool split = Epi::kSpmv && use_split(A);
+    const bool split = Epi::kSpmv && use_split(A, v.nlist);
     const int nw = v.nlist < 2 * 148 ? 24 : SPLIT_WARPS;
     const int bs = split ? nw * 32 : ROWS_BLOCK;
     unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);
@@ -314,6 +316,7 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     AMGP_TRY(halo_exchange_end(ctx, A));
     v.nown = h.nown;
     v.xh = h.halo;
+    v.xh_stride = p2p ? h.nhalo : 0;  // p2p halo: double-buffered by exchange parity
     v.nrecvp = nrecvp;
     if (p2p && h.n_boundary > 0) {  // the boundary launch completes the exchange itself
         v.complete = 1;

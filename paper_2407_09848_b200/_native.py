@@ -15,6 +15,7 @@ import contextlib
 import ctypes as C
 import os
 import threading
+import warnings
 
 import numpy as np
 
@@ -240,7 +241,10 @@ def to_device(a, c=None, copy=False):
         t.record_stream(c.stream)
         return t
     arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
-    host = torch.from_numpy(arr)
+    with warnings.catch_warnings():
+        # read-only arrays are only read (pinned copy / H2D upload)
+        warnings.simplefilter("ignore", UserWarning)
+        host = torch.from_numpy(arr)
     if host.numel() * 8 >= (1 << 16):
         host = host.pin_memory()
     return host.to(c.device, non_blocking=True)

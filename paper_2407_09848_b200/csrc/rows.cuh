@@ -307,6 +307,26 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
         }
         return launch_view(ctx, A, v, xg, epi);
     };
+    // a matrix with fewer slices than two per SM is launch-latency bound:
+    // splitting it would pay two dependent launches to hide an exchange the
+    // interior is too short to cover, so it runs as ONE halo-aware launch
+    // over all its slices after the exchange
+    if (A->nslices < 2 * 148) {
+        AMGP_TRY(halo_exchange_end(ctx, A));
+        v.slist = nullptr;
+        v.nruns = 1;
+        v.run_s0[0] = 0;
+        v.run_end[0] = v.nlist = A->nslices;
+        v.nown = h.nown;
+        v.xh = h.halo;
+        v.xh_stride = p2p ? h.nhalo : 0;
+        if (p2p && A->nslices > 0) {
+            v.complete = 1;
+            return launch_view(ctx, A, v, xg, epi);
+        }
+        if (A->nslices > 0) AMGP_TRY(launch_view(ctx, A, v, xg, epi));
+        return halo_exchange_done(ctx, A);
+    }
     // interior slices have no halo column (slice_maxcol < nown): plain gather
     v.nown = INT64_MAX;
     v.xh = nullptr;

@@ -37,14 +37,12 @@ def free_port():
     return p
 
 
-@pytest.mark.parametrize("transport", ["nccl", "p2p", "p2p_fused"])
-@pytest.mark.parametrize("graph", [False, True])
-def test_dist_check_two_gpus(graph, transport):
-    if ngpus() < 2:
-        pytest.skip("needs 2 GPUs")
-    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+def run_dist_check(nproc, grid, graph, transport):
+    if ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
            "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
-           os.path.join(REPO, "tools", "dist_check.py"), "--grid", "24"]
+           os.path.join(REPO, "tools", "dist_check.py"), "--grid", str(grid)]
     if graph:
         cmd.append("--graph")
     env = dict(os.environ)
@@ -54,7 +52,23 @@ def test_dist_check_two_gpus(graph, transport):
         env["AMGP_P2P_FUSED"] = "1"
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
-    assert len(lines) == 2, p.stdout[-2000:] + p.stderr[-2000:]
+    assert len(lines) == nproc, p.stdout[-2000:] + p.stderr[-2000:]
     for rec in lines:
         assert rec["ok"], rec
     assert p.returncode == 0
+
+
+@pytest.mark.parametrize("transport", ["nccl", "p2p", "p2p_fused"])
+@pytest.mark.parametrize("graph", [False, True])
+def test_dist_check_two_gpus(graph, transport):
+    # 24^3: every distributed matrix has < 2 slices per SM per rank -> the
+    # single halo-aware launch after the exchange (rows.cuh launch_rows)
+    run_dist_check(2, 24, graph, transport)
+
+
+@pytest.mark.parametrize("nproc", [2, 4])
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
+def test_dist_check_split_launches(nproc, transport):
+    # 48^3: the fine level holds >= 2 slices per SM per rank -> interior
+    # launch, exchange, boundary launch
+    run_dist_check(nproc, 48, True, transport)

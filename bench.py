@@ -489,7 +489,7 @@ def run_b200(args):
             "hbm_frac": value / ws / peak,
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_kind": peak_kind,
-                         "kernel": "k_cheb4_step<false,false,false> (middle degree step)",
+                         "kernel": "k_thread_rows<Cheb4Step<0,0,0>,0> (cheb4 middle degree step)",
                          "bytes_per_launch": mb, "ms_per_launch": t_mid,
                          "traffic": (traffic or {}).get("bytes_per_launch")},
             "mid_step_ms": mids,

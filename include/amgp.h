@@ -221,6 +221,58 @@ double amgp_setup_blas_dot(int64_t n, const double *x, const double *y, int thre
 int amgp_setup_spmv(int64_t n, const int64_t *row_ptr, const int64_t *col_idx,
                     const double *values, const double *x, double *y);
 
+/* ---- device hierarchy setup (amg.py:97-287 on the GPU; dsetup.cu) --------
+ * Device pointers.  Row-producing calls follow a count/fill protocol: with
+ * row_ptr == NULL they write each output row's entry count to row_cnt; with
+ * row_ptr (exclusive prefix sums of those counts) they write the rows,
+ * sorted by column, exact zeros dropped.  Columns of produced rows are
+ * global int64 indices; A operands are SELL matrices with local columns
+ * (own entries [0, nown), halo after, see amgp_mat_set_halo). */
+/* scipy csr_diagonal of the own rows (amg.py:221,267 A.diagonal()) */
+int amgp_ds_diag(amgp_mat *A, double *d);
+/* amg.py:115-121 strength test, own columns only (decoupled aggregation;
+ * every column is own on one GPU): strong neighbours j != i with
+ * |a_ij| >= theta sqrt(|a_ii a_jj|), in row order.  rows: optional list of
+ * rows (nlist of them); off == NULL: cnt[t] = list length; else write the
+ * int32 local columns at off[t] (and |a_ij| to sabs unless NULL). */
+int amgp_ds_strength(amgp_mat *A, const double *d, double theta, int64_t nown, const int64_t *rows,
+                     int64_t nlist, const int64_t *off, int64_t *cnt, int32_t *scol, double *sabs);
+/* numpy float64 dots x.y, x.x, y.y in OpenBLAS 0.3.30 SkylakeX ddot order
+ * with `threads` BLAS threads (== amgp_setup_blas_dot); out_host[3] */
+int amgp_ds_blas_dot3(amgp_ctx *ctx, int64_t n, const double *x, const double *y, int threads,
+                      double *out_host);
+/* amg.py:194-216 estimate_lambda_max: v (own rows) holds the start vector
+ * and is overwritten; the SpMV exchanges A's halo; fold_ranks: per-rank dots
+ * folded in rank order across the communicator (row-distributed A). */
+int amgp_ds_lambda_max(amgp_ctx *ctx, amgp_mat *A, const double *d, double *v, int iters, int threads,
+                       int fold_ranks, double *lam);
+/* amg.py:219-226 smooth_prolongator rows of A's own rows (smooth == 0: the
+ * tentative P_hat); agg_own / agg_halo: global coarse index of every own /
+ * halo column. */
+int amgp_ds_prolongator(amgp_mat *A, const double *d, const int64_t *agg_own, const int64_t *agg_halo,
+                        double omega, int smooth, const int64_t *row_ptr, int64_t *row_cnt, int64_t *col,
+                        double *val);
+/* scipy csr_matmat C = A_side B, per-entry order of the A-side rows (the
+ * Galerkin products of amg.py:229-235).  A-side: A_sell (local column c =
+ * B row c - b_off) or CSR (a_rp, a_col, a_val); output row t = A-side row
+ * a_rows[t] (NULL: t), nout rows. */
+int amgp_ds_spgemm(amgp_ctx *ctx, const amgp_mat *A_sell, const int64_t *a_rp, const int64_t *a_col,
+                   const double *a_val, const int64_t *a_rows, int64_t nout, const int64_t *b_rp,
+                   const int64_t *b_col, const double *b_val, int64_t b_off, const int64_t *row_ptr,
+                   int64_t *row_cnt, int64_t *c_col, double *c_val);
+/* amg.py:234 (G + G^T) * 0.5 from the sorted rows of G and G^T */
+int amgp_ds_symmetrize(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, const int64_t *g_col, const double *g_val,
+                       const int64_t *t_rp, const int64_t *t_col, const double *t_val, const int64_t *row_ptr,
+                       int64_t *row_cnt, int64_t *col, double *val);
+/* SELL-32 matrix from a device CSR with local int64 columns < 2^31 */
+int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *row_ptr,
+                       const int64_t *col, const double *val, amgp_mat **out);
+int amgp_mat_nown(const amgp_mat *A, int64_t *nown);
+/* host greedy passes of amg.py:124-148 over device-computed strength lists */
+int amgp_setup_sa_pass1(int64_t n, const int64_t *srp, const int32_t *scol, int64_t *agg, int64_t *n_agg);
+int amgp_setup_sa_pass2(int64_t nleft, const int64_t *rows, const int64_t *lrp, const int32_t *lcol,
+                        const double *labs, int64_t *agg, int64_t *n_agg);
+
 #ifdef __cplusplus
 }
 #endif

@@ -107,6 +107,18 @@ _SIGS = {
                                        C.POINTER(_VP)]),
     "amgp_setup_spmv": (C.c_int, [C.c_int64, _P64, _P64, _PD, _PD, _PD]),
     "amgp_setup_blas_dot": (C.c_double, [C.c_int64, _PD, _PD, C.c_int]),
+    "amgp_ds_diag": (C.c_int, [_VP, _VP]),
+    "amgp_ds_strength": (C.c_int, [_VP, _VP, C.c_double, C.c_int64, _VP, C.c_int64, _VP, _VP, _VP, _VP]),
+    "amgp_ds_blas_dot3": (C.c_int, [_VP, C.c_int64, _VP, _VP, C.c_int, _PD]),
+    "amgp_ds_lambda_max": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int, C.c_int, C.c_int, _PD]),
+    "amgp_ds_prolongator": (C.c_int, [_VP, _VP, _VP, _VP, C.c_double, C.c_int, _VP, _VP, _VP, _VP]),
+    "amgp_ds_spgemm": (C.c_int, [_VP, _VP, _VP, _VP, _VP, _VP, C.c_int64, _VP, _VP, _VP, C.c_int64,
+                                  _VP, _VP, _VP, _VP]),
+    "amgp_ds_symmetrize": (C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP]),
+    "amgp_mat_from_dcsr": (C.c_int, [_VP, C.c_int64, C.c_int64, _VP, _VP, _VP, C.POINTER(_VP)]),
+    "amgp_mat_nown": (C.c_int, [_VP, _P64]),
+    "amgp_setup_sa_pass1": (C.c_int, [C.c_int64, _P64, C.POINTER(C.c_int32), _P64, _P64]),
+    "amgp_setup_sa_pass2": (C.c_int, [C.c_int64, _P64, _P64, C.POINTER(C.c_int32), _PD, _P64, _P64]),
     "amgp_comm_unique_id": (C.c_int, [C.c_char_p]),
     "amgp_ctx_init_comm": (C.c_int, [_VP, C.c_int, C.c_int, C.c_char_p]),
     "amgp_ctx_comm_info": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),

@@ -175,17 +175,46 @@ def hierarchy_from_levels(levels, smoother, coarse_solver="l1_jacobi", coarse_sw
 
 
 def build_hierarchy(A, coarsening=None, smoother=None, max_levels=10, min_coarse_size=200,
-                    coarse_solver="l1_jacobi", coarse_sweeps=30):
+                    coarse_solver="l1_jacobi", coarse_sweeps=30, setup=None):
     """Build levels until the coarse size or level cap is hit (amg.py:238-287).
 
-    Host setup in native C++ (csrc/setup.cpp), bit-exact with the reference.
+    setup="device" (default when a GPU is present): the GPU setup of
+    dsetup.py -- levels stay on the device (their host views download on
+    demand).  setup="host": the native C++ host restatement (csrc/setup.cpp).
+    Both are bitwise the reference's hierarchy.
     """
-    from . import setup as _setup
-
     coarsening = coarsening or CoarseningConfig()
     smoother = smoother or PolySmootherConfig(family="opt_cheb1", degree=4)
-    return _setup.build_hierarchy(A, coarsening, smoother, max_levels, min_coarse_size,
-                                  coarse_solver, coarse_sweeps)
+    if setup is None:
+        setup = "device" if _gpu_present() else "host"
+    if setup == "host":
+        from . import setup as _setup
+
+        return _setup.build_hierarchy(A, coarsening, smoother, max_levels, min_coarse_size,
+                                      coarse_solver, coarse_sweeps)
+    if setup != "device":
+        raise ValueError(f"unknown setup {setup!r}")
+    from . import dsetup
+
+    dl, stagnated = dsetup.build_levels(A, coarsening, max_levels=max_levels,
+                                        min_coarse_size=min_coarse_size)
+    levels = []
+    for L in dl:
+        lv = Level(A=L.A, M=L1JacobiData(m_diag=L.m), smoother=smoother, P=L.P,
+                   n_aggregates=L.n_aggregates if L.P is not None else 0)
+        lv._Pt = L.R
+        levels.append(lv)
+    return AmgHierarchy(levels=levels, coarse_solver=coarse_solver, coarse_sweeps=coarse_sweeps,
+                        stagnated=stagnated)
+
+
+def _gpu_present():
+    try:
+        import torch
+
+        return torch.cuda.is_available()
+    except Exception:
+        return False
 
 
 def vcycle_apply(h, r, _level=0):

@@ -57,7 +57,7 @@ extern "C" int amgp_sell_pack_host(int64_t nrows, const int64_t *row_ptr,
     return AMGP_OK;
 }
 
-static int mat_alloc(amgp_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, int64_t ns,
+int mat_alloc(amgp_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, int64_t ns,
                      int64_t stored, amgp_mat **out) {
     amgp_mat *A = new amgp_mat();
     A->ctx = ctx;

@@ -413,6 +413,54 @@ int amgp_setup_sa_aggregate(int64_t n, const int64_t *rp, const int64_t *ci, con
     return AMGP_OK;
 }
 
+// amg.py:124-133, the seeding pass of sa_aggregate over precomputed strength
+// lists (the device setup computes them: strong neighbours of row i in row
+// order, j != i, own columns).  agg is reset to -1 first.
+int amgp_setup_sa_pass1(int64_t n, const int64_t *srp, const int32_t *scol, int64_t *agg,
+                        int64_t *n_agg_out) {
+    if (n < 0 || !srp || !agg || !n_agg_out) return amgp_fail(AMGP_EINVAL, "sa_pass1: bad argument");
+    std::fill(agg, agg + n, -1);
+    int64_t n_agg = 0;
+    for (int64_t i = 0; i < n; i++) {
+        if (agg[i] >= 0) continue;
+        int cnt = 0;
+        for (int64_t jj = srp[i]; jj < srp[i + 1] && cnt < 2; jj++) cnt += agg[scol[jj]] < 0;
+        if (cnt < 2) continue;
+        agg[i] = n_agg;
+        for (int64_t jj = srp[i]; jj < srp[i + 1]; jj++)
+            if (agg[scol[jj]] < 0) agg[scol[jj]] = n_agg;
+        n_agg++;
+    }
+    *n_agg_out = n_agg;
+    return AMGP_OK;
+}
+
+// amg.py:134-148, the leftover pass: rows[] (ascending) are the rows the
+// seeding pass left unaggregated, each with its strength list and |a_ij|;
+// a row joins the aggregate of its strongest aggregated strong neighbour
+// (strict >, first wins), else becomes a singleton.
+int amgp_setup_sa_pass2(int64_t nleft, const int64_t *rows, const int64_t *lrp, const int32_t *lcol,
+                        const double *labs, int64_t *agg, int64_t *n_agg) {
+    if (nleft < 0 || (nleft && (!rows || !lrp)) || !agg || !n_agg)
+        return amgp_fail(AMGP_EINVAL, "sa_pass2: bad argument");
+    for (int64_t t = 0; t < nleft; t++) {
+        const int64_t i = rows[t];
+        if (agg[i] >= 0) continue;
+        int64_t best = -1;
+        double best_w = -1.0;
+        for (int64_t jj = lrp[t]; jj < lrp[t + 1]; jj++) {
+            const int64_t j = lcol[jj];
+            if (agg[j] >= 0 && labs[jj] > best_w) {
+                best = agg[j];
+                best_w = labs[jj];
+            }
+        }
+        if (best >= 0) agg[i] = best;
+        else agg[i] = (*n_agg)++;
+    }
+    return AMGP_OK;
+}
+
 // amg.py:152-191
 int amgp_setup_matching_aggregate(int64_t n0, const int64_t *rp, const int64_t *ci,
                                   const double *v, int sweeps, int64_t *agg_out,

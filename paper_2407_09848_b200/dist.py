@@ -213,6 +213,13 @@ def poisson3d_block(m, comm, stencil=7):
                     recv_cols=[])
     attach_halo(D, plan)
     D.global_rows = (lo, hi)
+    D.n_global = n
+    D.row_partition = off
+    # global ids of the halo columns in local order (device setup, dsetup.py)
+    import torch
+
+    D.halo_g = torch.cat([torch.arange(a, b, dtype=torch.int64) for _, a, b in segs]).to(comm.ctx.device) \
+        if segs else torch.zeros(0, dtype=torch.int64, device=comm.ctx.device)
     return D
 
 
@@ -259,14 +266,15 @@ def share_hierarchy(h_or_builder, comm_rank, barrier, cache=None):
         path = cache if cache is not None else os.path.join(base, name)
         shutil.rmtree(path, ignore_errors=True)
         os.makedirs(path)
-        arrs = {"nlev": np.array([len(h.levels)]), "coarse_sweeps": np.array([h.coarse_sweeps])}
+        arrs = {"nlev": np.array([len(h.levels)]), "coarse_sweeps": np.array([h.coarse_sweeps]),
+                "coarse_solver": np.array([h.coarse_solver])}
         for l, lv in enumerate(h.levels):
             for key, M in (("A", lv.A), ("P", lv.P), ("R", lv.restrict_op() if lv.P is not None else None)):
                 if M is None:
                     continue
                 arrs[f"{key}{l}_shape"] = np.array([M.nrows, M.ncols])
                 arrs[f"{key}{l}_rp"], arrs[f"{key}{l}_ci"], arrs[f"{key}{l}_v"] = M.row_ptr, M.col_idx, M.values
-            arrs[f"M{l}"] = np.asarray(lv.M.m_diag)
+            arrs[f"M{l}"] = N.to_host(lv.M.m_diag) if N.is_torch(lv.M.m_diag) else np.asarray(lv.M.m_diag)
         for k, a in arrs.items():
             np.save(os.path.join(path, k + ".npy"), a)
         open(os.path.join(path, "complete"), "w").close()
@@ -294,13 +302,10 @@ class DistHierarchy:
     """This rank's slice of an AMG hierarchy on its GPU (libamgp hierarchy
     with halo-exchanging matrices).  Vectors are the rank's fine-level rows."""
 
-    def __init__(self, d, comm, smoother, replicate_below=20000, coarse_sweeps=30, use_graph=False):
-        from .amg import Level, AmgHierarchy, _smoother_key
-        from .smoothers import L1JacobiData
-
-        self.comm = comm
+    def __init__(self, d, comm, smoother, replicate_below=20000, coarse_sweeps=None, use_graph=False,
+                 coarse_solver=None):
+        """Partition a shared global hierarchy (share_hierarchy) by rows."""
         c = comm.ctx
-        self.ctx = c
         L = int(d["nlev"][0])
         A_glob = [_mat(d, f"A{l}") for l in range(L)]
 
@@ -308,11 +313,9 @@ class DistHierarchy:
             levels = [type("Lv", (), {"A": a}) for a in A_glob]
 
         parts = level_partitions(_H, comm.size, replicate_below)
-        self.parts = parts
         me = comm.rank
-        self.dev = []   # keep device objects alive
-        self.plans = []
         As, Ms, Ps, Rs = [], [], [], []
+        plans = []
         for l in range(L):
             Al, plan = localize(A_glob[l], parts[l], parts[l], me)
             DA = attach_halo(DeviceMatrix.from_csr(Al, c), plan)
@@ -320,25 +323,72 @@ class DistHierarchy:
             m = N.to_device(np.ascontiguousarray(d[f"M{l}"][lo:hi]), c)
             As.append(DA)
             Ms.append(m)
-            self.plans.append(plan)
+            plans.append(plan)
             if l < L - 1:
                 Pl, pplan = localize(_mat(d, f"P{l}"), parts[l], parts[l + 1], me)
                 Rl, rplan = localize(_mat(d, f"R{l}"), parts[l + 1], parts[l], me)
                 Ps.append(attach_halo(DeviceMatrix.from_csr(Pl, c), pplan))
                 Rs.append(attach_halo(DeviceMatrix.from_csr(Rl, c), rplan))
+        # the coarse solve of the shared hierarchy (amg.py:65-66), unless overridden
+        if coarse_solver is None:
+            coarse_solver = str(d["coarse_solver"][0]) if "coarse_solver" in d else "l1_jacobi"
+        if coarse_sweeps is None:
+            coarse_sweeps = int(d["coarse_sweeps"][0]) if "coarse_sweeps" in d else 30
+        row_range = (int(parts[0][me]), int(parts[0][me + 1])) if parts[0] is not None else (0, As[0].nrows)
+        self._setup(comm, As, Ms, Ps, Rs, parts, row_range, smoother, coarse_solver, coarse_sweeps, use_graph,
+                    coarse_A=A_glob[-1])
+        self.plans = plans
+
+    @classmethod
+    def from_levels(cls, levels, comm, smoother, coarse_solver="l1_jacobi", coarse_sweeps=30, use_graph=False):
+        """Hierarchy from the per-rank levels of the distributed device setup
+        (dsetup.build_levels)."""
+        self = cls.__new__(cls)
+        As = [L.A for L in levels]
+        Ms = [L.m for L in levels]
+        Ps = [L.P for L in levels[:-1]]
+        Rs = [L.R for L in levels[:-1]]
+        parts = [L.off for L in levels]
+        row_range = (levels[0].lo, levels[0].hi)
+        self._setup(comm, As, Ms, Ps, Rs, parts, row_range, smoother, coarse_solver, coarse_sweeps, use_graph,
+                    coarse_A=levels[-1].A if levels[-1].off is None else None)
+        self.levels = levels
+        return self
+
+    def _setup(self, comm, As, Ms, Ps, Rs, parts, row_range, smoother, coarse_solver, coarse_sweeps, use_graph,
+               coarse_A=None):
+        self.comm = comm
+        c = comm.ctx
+        self.ctx = c
+        L = len(As)
+        self.parts = parts
         self.As, self.Ms, self.Ps, self.Rs = As, Ms, Ps, Rs
         self.n_local = As[0].nrows
-        self.row_range = (int(parts[0][me]), int(parts[0][me + 1])) if parts[0] is not None else (0, As[0].nrows)
+        self.row_range = row_range
         Aa = (N._VP * L)(*[a.handle for a in As])
         Ma = (N._VP * L)(*[m.data_ptr() for m in Ms])
         Pa = (N._VP * max(L - 1, 1))(*[p.handle for p in Ps])
         Ra = (N._VP * max(L - 1, 1))(*[r.handle for r in Rs])
+        if coarse_solver not in N.COARSE_CODES or coarse_solver == "smoother":
+            raise ValueError(f"unknown coarse solver {coarse_solver!r}")
+        if coarse_solver == "dense_direct" and (parts[-1] is not None and comm.size > 1):
+            raise ValueError("dense_direct needs a replicated coarsest level")
         handle = N._VP()
         with c.scope():
-            N.check(N.lib().amgp_hier_create(c.handle, L, Aa, Ma, Pa, Ra, N.COARSE_CODES["l1_jacobi"],
+            N.check(N.lib().amgp_hier_create(c.handle, L, Aa, Ma, Pa, Ra, N.COARSE_CODES[coarse_solver],
                                              int(coarse_sweeps), C.byref(handle)))
             N.check(N.lib().amgp_hier_use_graph(handle, int(use_graph)))
         self.handle = handle
+        if coarse_solver == "dense_direct":
+            Ad = coarse_A.to_dense()
+            try:
+                Lf = np.linalg.cholesky(Ad)
+            except np.linalg.LinAlgError as exc:
+                raise ValueError("matrix is not positive definite") from exc
+            Lc = np.ascontiguousarray(Lf.T)
+            N.check(N.lib().amgp_hier_set_coarse_cholesky(handle, Lc.ctypes.data_as(N._PD)))
+        self.coarse_solver = coarse_solver
+        self.coarse_sweeps = coarse_sweeps
         self.set_smoother(smoother)
 
     def set_smoother(self, cfg):

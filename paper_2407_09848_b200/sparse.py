@@ -49,6 +49,7 @@ class DeviceMatrix:
         self.nnz = int(nnz)
         self.row_offset = int(row_offset)
         self._m = None
+        self._host = None
 
     @classmethod
     def from_csr(cls, A, c=None):
@@ -92,6 +93,37 @@ class DeviceMatrix:
             N.check(N.lib().amgp_mat_to_csr(self.handle, rp.ctypes.data_as(N._P64),
                                             ci.ctypes.data_as(N._P64), v.ctypes.data_as(N._PD)))
         return CsrMatrix(self.nrows, self.ncols, rp, ci, v)
+
+    # -- host views (reference CsrMatrix fields; downloaded once, on demand)
+    def host(self):
+        """The matrix as a host CsrMatrix (local columns), cached."""
+        if getattr(self, "_host", None) is None:
+            self._host = self.to_csr()
+        return self._host
+
+    @property
+    def row_ptr(self):
+        return self.host().row_ptr
+
+    @property
+    def col_idx(self):
+        return self.host().col_idx
+
+    @property
+    def values(self):
+        return self.host().values
+
+    def to_scipy(self):
+        return self.host().to_scipy()
+
+    def to_dense(self):
+        return self.host().to_dense()
+
+    def diagonal(self):
+        return self.host().diagonal()
+
+    def transpose(self):
+        return self.host().transpose()
 
     def l1_diag(self):
         """Device l1-Jacobi diagonal (reference smoothers.py:38-49, same bits)."""

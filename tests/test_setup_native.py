@@ -42,7 +42,7 @@ KINDS = {"sa": "smoothed_aggregation", "mt": "pairwise_matching"}
 def test_hierarchy_arrays_bitwise(prefix, m):
     d = golden("hier_small.npz")
     A, _ = P.poisson3d(m)
-    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=KINDS[prefix[:2]]),
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=KINDS[prefix[:2]]), setup="host",
                           smoother=P.PolySmootherConfig(family="cheb4", degree=4))
     L = int(d[prefix + "_nlev"][0])
     assert len(h.levels) == L
@@ -59,7 +59,7 @@ def test_hierarchy_arrays_bitwise(prefix, m):
 def test_hierarchy_digests(m, kind):
     ref = golden("hashes.json")[f"p3d{m}_{kind}"]
     A, _ = P.poisson3d(m)
-    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind), setup="host",
                           smoother=P.PolySmootherConfig(family="cheb4", degree=4))
     assert len(h.levels) == len(ref["levels"])
     for l, (lv, lr) in enumerate(zip(h.levels, ref["levels"])):
@@ -76,7 +76,7 @@ def test_hierarchy_digests_27point(m, kind):
     """27-point stencil (BASELINE configs[4]): native setup == reference setup."""
     ref = golden("hashes27.json")[f"p27_{m}"][kind]
     A, _ = P.poisson3d_27(m)
-    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind), setup="host",
                           smoother=P.PolySmootherConfig(family="opt_cheb1", degree=3))
     assert len(h.levels) == len(ref["levels"])
     for l, (lv, lr) in enumerate(zip(h.levels, ref["levels"])):
@@ -139,7 +139,7 @@ def test_blas_dot_emulation_matches_numpy(threads):
 
 def test_operator_complexity_and_summary():
     A, _ = P.poisson3d(8)
-    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind="pairwise_matching"))
+    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind="pairwise_matching"), setup="host")
     assert h.operator_complexity() <= 3.0
     s = h.summary()
     assert s["levels"][0]["size"] == 512

@@ -299,7 +299,9 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
         return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     };
     const bool fcg = variant == AMGP_FCG;
-    const bool dist = ctx->comm != nullptr && ctx->nranks > 1;
+    // row-distributed solve: the fine matrix carries a halo plan (a single-GPU
+    // solve on a multi-rank context stays local)
+    const bool dist = ctx->comm != nullptr && ctx->nranks > 1 && A->halo != nullptr;
     cudaStream_t st = ctx->stream;
     double *sc = ctx->scalars, *hs = ctx->host_scalars;
 

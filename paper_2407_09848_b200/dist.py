@@ -220,6 +220,7 @@ def poisson3d_block(m, comm, stencil=7):
 
     D.halo_g = torch.cat([torch.arange(a, b, dtype=torch.int64) for _, a, b in segs]).to(comm.ctx.device) \
         if segs else torch.zeros(0, dtype=torch.int64, device=comm.ctx.device)
+    D.col_map = torch.cat([torch.arange(lo, hi, dtype=torch.int64, device=comm.ctx.device), D.halo_g])
     return D
 
 

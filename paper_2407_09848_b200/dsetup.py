@@ -151,7 +151,7 @@ class Exchanger:
 
         torch = _torch()
         out = torch.empty(self.nhalo, dtype=x.dtype, device=x.device)
-        dist.all_to_all_single(out, x[self.send_idx].contiguous(), self.recv_counts, self.send_counts)
+        _a2a(out, x[self.send_idx].contiguous(), self.recv_counts, self.send_counts)
         return out
 
     def rows(self, m):
@@ -162,18 +162,42 @@ class Exchanger:
         dev = m.rp.device
         lens = m.lens()[self.send_idx]
         rl = torch.empty(self.nhalo, dtype=torch.int64, device=dev)
-        dist.all_to_all_single(rl, lens.contiguous(), self.recv_counts, self.send_counts)
+        _a2a(rl, lens.contiguous(), self.recv_counts, self.send_counts)
         ent_send = _split_sums(lens, self.send_counts)
         ent_recv = _split_sums(rl, self.recv_counts)
         idx = _ragged(m.rp[self.send_idx], lens)
         col = torch.empty(sum(ent_recv), dtype=torch.int64, device=dev)
         val = torch.empty(sum(ent_recv), dtype=torch.float64, device=dev)
-        dist.all_to_all_single(col, m.col[idx].contiguous(), ent_recv, ent_send)
-        dist.all_to_all_single(val, m.val[idx].contiguous(), ent_recv, ent_send)
+        _a2a(col, m.col[idx].contiguous(), ent_recv, ent_send)
+        _a2a(val, m.val[idx].contiguous(), ent_recv, ent_send)
         rp = torch.zeros(self.nhalo + 1, dtype=torch.int64, device=dev)
         if self.nhalo:
             torch.cumsum(rl, 0, out=rp[1:])
         return DCsr(rp, col, val)
+
+
+def _a2a(out, inp, out_splits=None, in_splits=None):
+    """all_to_all_single; gloo process groups get host copies."""
+    import torch.distributed as dist
+
+    if dist.get_backend() == "gloo" and out.is_cuda:
+        o = out.cpu()
+        dist.all_to_all_single(o, inp.cpu(), out_splits, in_splits)
+        out.copy_(o)
+    else:
+        dist.all_to_all_single(out, inp, out_splits, in_splits)
+
+
+def _all_gather(outs, t):
+    import torch.distributed as dist
+
+    if dist.get_backend() == "gloo" and t.is_cuda:
+        oc = [o.cpu() for o in outs]
+        dist.all_gather(oc, t.cpu())
+        for o, h in zip(outs, oc):
+            o.copy_(h)
+    else:
+        dist.all_gather(outs, t)
 
 
 def _split_sums(x, counts):
@@ -200,7 +224,7 @@ def _all_gather_ints(vals, dev):
     torch = _torch()
     t = torch.as_tensor(np.asarray(vals, dtype=np.int64), device=dev)
     out = [torch.empty_like(t) for _ in range(dist.get_world_size())]
-    dist.all_gather(out, t)
+    _all_gather(out, t)
     return np.stack([o.cpu().numpy() for o in out])
 
 
@@ -210,7 +234,7 @@ def _all_to_all_counts(counts, dev):
     torch = _torch()
     t = torch.as_tensor(np.asarray(counts, dtype=np.int64), device=dev)
     out = torch.empty_like(t)
-    dist.all_to_all_single(out, t)
+    _a2a(out, t)
     return out.cpu().tolist()
 
 
@@ -235,7 +259,7 @@ def make_halo(cols, lo, hi, off, me):
     recv_counts = torch.bincount(owner, minlength=nranks).cpu().tolist() if halo_g.numel() else [0] * nranks
     send_counts = _all_to_all_counts(recv_counts, dev)
     need = torch.empty(sum(send_counts), dtype=torch.int64, device=dev)
-    dist.all_to_all_single(need, halo_g.contiguous(), send_counts, recv_counts)
+    _a2a(need, halo_g.contiguous(), send_counts, recv_counts)
     send_idx = need - lo
     peers = [q for q in range(nranks) if q != me and (recv_counts[q] or send_counts[q])]
     plan = HaloPlan(
@@ -398,7 +422,7 @@ def _gather_rows(m, comm_size):
         buf = torch.zeros(max(mx, 1), dtype=dtype, device=dev)
         buf[: x.numel()] = x
         outs = [torch.empty_like(buf) for _ in range(comm_size)]
-        dist.all_gather(outs, buf)
+        _all_gather(outs, buf)
         return torch.cat([o[: int(cnt)] for o, cnt in zip(outs, counts)])
 
     lens = gather(m.lens(), nr, torch.int64)
@@ -478,6 +502,11 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
     me = comm.rank if comm is not None else 0
     budget = galerkin_budget or int(os.environ.get("AMGP_GALERKIN_BUDGET", str(1 << 28)))
     t_start = time.perf_counter()
+
+    if trace is None and os.environ.get("AMGP_SETUP_TRACE"):
+        import sys
+
+        trace = lambda s: print(f"[rank {me}] {s}", file=sys.stderr, flush=True)  # noqa: E731
 
     def log(msg):
         if trace:
@@ -566,12 +595,16 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
             R_csr = _csr_from_entries(na, J, I, Pext.val[keep], J * max(L.n, 1) + ext_g[I])
             del erow, keep, J, I
             R = _attach(_sell(c, R_csr, A.ncols), L.plan if dist_l else None)
+            R.col_map, R.row_lo = (ext_g if dist_l else None), clo
             # P as a device matrix (columns: coarse level, localised when it stays distributed)
             if dist_l and not replicate_next:
-                pl, _, pplan, _ = make_halo(Prow.col, clo, chi, coff, me)
+                pl, phg, pplan, _ = make_halo(Prow.col, clo, chi, coff, me)
                 P = _attach(_sell(c, DCsr(Prow.rp, pl, Prow.val), pplan.nown + int(pplan.recv_cnt.sum())), pplan)
+                P.col_map = torch.cat([torch.arange(clo, chi, dtype=torch.int64, device=dev), phg])
             else:
                 P = _sell(c, Prow, nc)
+                P.col_map = None
+            P.row_lo = L.lo
             # -- Galerkin (amg.py:229-235)
             if dist_l:
                 Cm = _spgemm(c, n_loc, Pext, a_sell=A)
@@ -596,9 +629,9 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
                 recv_counts = _all_to_all_counts(send_counts, dev)
                 tr, tc, tv = (torch.empty(sum(recv_counts), dtype=dt, device=dev)
                               for dt in (torch.int64, torch.int64, torch.float64))
-                dist.all_to_all_single(tr, G.col[order].contiguous(), recv_counts, send_counts)
-                dist.all_to_all_single(tc, Gr[order].contiguous(), recv_counts, send_counts)
-                dist.all_to_all_single(tv, G.val[order].contiguous(), recv_counts, send_counts)
+                _a2a(tr, G.col[order].contiguous(), recv_counts, send_counts)
+                _a2a(tc, Gr[order].contiguous(), recv_counts, send_counts)
+                _a2a(tv, G.val[order].contiguous(), recv_counts, send_counts)
                 del dest, order
             else:
                 tr, tc, tv = G.col, Gr, G.val
@@ -625,8 +658,10 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
                 Afull = _gather_rows(Ac, size)
                 R_g = DCsr(R_csr.rp, ext_g[R_csr.col], R_csr.val)
                 Rfull = _gather_rows(R_g, size)
-                rl, _, rplan, _ = make_halo(Rfull.col, L.lo, L.hi, L.off, me)
+                rl, rhg, rplan, _ = make_halo(Rfull.col, L.lo, L.hi, L.off, me)
                 L.R = _attach(_sell(c, DCsr(Rfull.rp, rl, Rfull.val), rplan.nown + sum(rplan.recv_cnt)), rplan)
+                L.R.col_map = torch.cat([torch.arange(L.lo, L.hi, dtype=torch.int64, device=dev), rhg])
+                L.R.row_lo = 0
                 del R, Rfull, R_g
                 nxt = DLevel(A=_sell(c, Afull, nc), n=nc, off=None, lo=0, hi=nc)
                 del Afull
@@ -636,6 +671,7 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
                 Aloc = DCsr(Ac.rp, al, Ac.val)
                 nxt = DLevel(A=_attach(_sell(c, Aloc, na + int(hg.numel())), aplan), n=nc, off=coff, lo=clo,
                              hi=chi, halo_g=hg, plan=aplan, exch=aex)
+                nxt.A.col_map = torch.cat([torch.arange(clo, chi, dtype=torch.int64, device=dev), hg])
                 del Aloc, al
             else:
                 L.R = R

@@ -237,120 +237,206 @@ def cpu_baseline(m):
     oracle.set_threads(1)
     return {"value": tot_b / tot_t / 1e9, "unit": "GB/s", "cores": threads, "kind": "port",
             "sample": f"{m}^3 fine level, opt_cheb1/cheb4/opt_cheb4 k=4, one apply each "
-                      f"({tot_t:.1f} s)"}
+                      f"({tot_t:.1f} s); the C restatement of the reference's smoother_apply "
+                      f"(oracle/amgp_oracle.c, pthreads row split), not the reference's "
+                      f"single-core Python, which cannot run on the GPU box"}
 
 
-def solve_bench(m, kind="smoothed_aggregation", cpu=True, stencil=7, k=4, cpu_family="opt_cheb1"):
-    """PCG + AMG V-cycle solve (BASELINE metric part 2) on poisson3d(m)
-    (7-point) or the 27-point stencil: native host setup, then per smoother
-    family (degree k) one device solve at rtol 1e-6 timed with CUDA events on
-    the library stream; the C oracle solves the same hierarchy on the host
-    (all cores) for the CPU column."""
+def mat_bytes(nrows, nnz):
+    return 12 * nnz + 4 * (nrows + 1)
+
+
+def vcycle_bytes(levels, k, family):
+    """Algorithmic HBM bytes of one V-cycle:
+    per level pre-smoother (x0 = 0: the first SpMV skipped), residual,
+    restriction, prolongation, post-smoother; coarsest: one pass of its
+    sweeps' data (the single-CTA solve keeps the level on chip).
+    levels: [(n, nnz_A, nnz_P, nnz_R, n_coarse)]"""
+    tot = 0
+    for i, (n, nnz, pnnz, rnnz, nc) in enumerate(levels):
+        A = mat_bytes(n, nnz)
+        if nc is None:
+            tot += A + 32 * n
+            continue
+        post = (A + 32 * n) * k if family == "l1_jacobi" else apply_bytes(n, nnz, k)
+        pre = post - (A + 8 * n)
+        tot += pre + post + (A + 24 * n) + (mat_bytes(nc, rnnz) + 8 * n + 8 * nc) + (mat_bytes(n, pnnz) + 16 * n + 8 * nc)
+    return tot
+
+
+def pcg_iter_bytes(n0, nnz0):
+    """PCG vector kernels + the SpMV of one iteration (pcg.cu K7 table)."""
+    return mat_bytes(n0, nnz0) + 104 * n0
+
+
+def _level_shapes(As, Ps, Rs):
+    out = []
+    for i, A in enumerate(As):
+        if i < len(Ps):
+            out.append((A.nrows, A.nnz, Ps[i].nnz, Rs[i].nnz, Rs[i].nrows))
+        else:
+            out.append((A.nrows, A.nnz, 0, 0, None))
+    return out
+
+
+def solve_roofline(shapes, k, family, iters, seconds, peak):
+    """Algorithmic GB/s of a whole solve: (iters + 1) V-cycles + iters PCG
+    iterations (+ the initial residual) over the measured solve time."""
+    n0, nnz0 = shapes[0][0], shapes[0][1]
+    byts = (iters + 1) * vcycle_bytes(shapes, k, family) + (iters + 1) * pcg_iter_bytes(n0, nnz0)
+    gbs = byts / seconds / 1e9
+    return {"bound": "hbm", "bytes": byts, "achieved": gbs, "peak": peak, "unit": "GB/s", "frac": gbs / peak,
+            "note": "per-level algorithmic bytes (12 nnz + 4 (n+1) per matrix + vector streams) over the "
+                    "device-timed solve; every rank's own rows at N > 1"}
+
+
+def solve_bench(m, kind="smoothed_aggregation", cpu=True, stencil=7, k=4, cpu_family="opt_cheb1",
+                families=("opt_cheb1", "cheb4", "opt_cheb4", "l1_jacobi")):
+    """PCG + AMG V-cycle solve (BASELINE metric part 2) on the m^3 7-point
+    (or 27-point) Poisson matrix generated on the GPU: device setup
+    (dsetup.py, bitwise the reference's hierarchy), then per smoother family
+    (degree k) one device solve at rtol 1e-6 timed with CUDA events on the
+    library stream; the C oracle solves the same hierarchy on the host (all
+    cores) for the CPU column."""
     import torch
 
     import paper_2407_09848_b200 as P
-    from paper_2407_09848_b200 import _native as N
 
-    A, b = (P.poisson3d if stencil == 7 else P.poisson3d_27)(m)
+    D0 = P.poisson3d_device(m, stencil)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
-                          smoother=P.PolySmootherConfig(family="opt_cheb1", degree=4))
+    h = P.build_hierarchy(D0, coarsening=P.CoarseningConfig(kind=kind),
+                          smoother=P.PolySmootherConfig(family="opt_cheb1", degree=k))
+    torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    t0 = time.perf_counter()
     D = h.device()
-    upload_s = time.perf_counter() - t0
     c = D.ctx
-    bd = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
+    n = D0.nrows
+    bd = torch.ones(n, dtype=torch.float64, device="cuda")
     cfg_k = P.KrylovConfig(tol=1e-6, itmax=1000)
-    out = {"m": m, "n": A.nrows, "stencil": stencil, "degree": k, "coarsening": kind,
-           "levels": [lv.A.nrows for lv in h.levels],
+    shapes = _level_shapes([lv.A for lv in h.levels], [lv.P for lv in h.levels[:-1]],
+                           [lv.restrict_op() for lv in h.levels[:-1]])
+    peak, _ = peaks()
+    out = {"m": m, "n": n, "stencil": stencil, "degree": k, "coarsening": kind,
+           "levels": [lv.A.nrows for lv in h.levels], "nnz": [lv.A.nnz for lv in h.levels],
            "operator_complexity": h.operator_complexity(), "setup_s": setup_s,
-           "upload_s": upload_s, "tol": 1e-6, "results": {}}
-    for fam in ("opt_cheb1", "cheb4", "opt_cheb4", "l1_jacobi"):
+           "setup": "device (dsetup.py; bitwise the reference hierarchy)", "tol": 1e-6, "results": {}}
+    for fam in families:
         cfg = P.PolySmootherConfig(family=fam, degree=k)
         for lv in h.levels:
             lv.smoother = cfg
         pre = P.as_vcycle_preconditioner(h)
-        P.solve(A, bd, precond=pre, cfg=cfg_k)  # warm-up (graph capture)
+        P.solve(D0, bd, precond=pre, cfg=cfg_k)  # warm-up (graph capture)
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(c.stream)
-        x, rep = P.solve(A, bd, precond=pre, cfg=cfg_k)
+        x, rep = P.solve(D0, bd, precond=pre, cfg=cfg_k)
         e1.record(c.stream)
         torch.cuda.synchronize()
+        sec = e0.elapsed_time(e1) / 1e3
         out["results"][fam] = {"iterations": rep.iterations, "final_relres": rep.final_relres,
-                               "solve_s": e0.elapsed_time(e1) / 1e3, "wall_s": rep.elapsed_s}
+                               "solve_s": sec, "wall_s": rep.elapsed_s,
+                               "roofline": solve_roofline(shapes, k, fam, rep.iterations, sec, peak)}
     if cpu:
         sys.path.insert(0, os.path.join(REPO, "oracle"))
         import oracle
 
-        lv = [{"A": (l.A.row_ptr, l.A.col_idx, l.A.values), "m": l.M.m_diag,
-               **({"P": (l.P.row_ptr, l.P.col_idx, l.P.values),
-                   "R": (l.restrict_op().row_ptr, l.restrict_op().col_idx, l.restrict_op().values)}
-                  if l.P is not None else {})} for l in h.levels]
+        lv = []
+        for l in h.levels:
+            Ah = l.A.host()
+            ent = {"A": (Ah.row_ptr, Ah.col_idx, Ah.values), "m": l.M.m_diag.cpu().numpy()}
+            if l.P is not None:
+                Ph, Rh = l.P.host(), l.restrict_op().host()
+                ent["P"] = (Ph.row_ptr, Ph.col_idx, Ph.values)
+                ent["R"] = (Rh.row_ptr, Rh.col_idx, Rh.values)
+            lv.append(ent)
         cfg = P.PolySmootherConfig(family=cpu_family, degree=k)
         beta = cfg.beta.beta if cfg.family == "opt_cheb4" else None
         oh = oracle.Hierarchy(lv, cpu_family, k, a=cfg.a or 0.0, beta=beta)
         threads = oracle.max_threads()
         oracle.set_threads(threads)
         t0 = time.perf_counter()
-        _, it, rr, conv, brk, _ = oracle.pcg(lv[0]["A"], np.ones(A.nrows), oh, tol=1e-6)
+        _, it, rr, conv, brk, _ = oracle.pcg(lv[0]["A"], np.ones(n), oh, tol=1e-6)
         out["cpu_" + cpu_family] = {"iterations": it, "final_relres": rr,
-                                "solve_s": time.perf_counter() - t0, "cores": threads,
-                                "kind": "port"}
+                                    "solve_s": time.perf_counter() - t0, "cores": threads,
+                                    "kind": "port (C oracle, same hierarchy)"}
         oracle.set_threads(1)
     return out
 
 
-def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, strong=False):
-    """PCG + AMG solve over all ranks: weak-scaled (BASELINE configs[3]
-    shape: global cube round(m_base N^(1/3))) or strong-scaled (configs[4]
-    shape: global cube m_base), hierarchy built once on rank 0 (native
-    setup) and shared, every level row-partitioned (coarse levels
-    replicated).  Returns (on every rank) iterations and max-over-ranks time."""
+def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, strong=False, replicate_below=20000):
+    """PCG + AMG solve over all ranks (also N = 1): weak-scaled (BASELINE
+    configs[3]: global cube round(m_base N^(1/3)), ~m_base^3 rows per GPU) or
+    strong-scaled (configs[4]: global cube m_base).  Each rank generates its
+    row block on its GPU and the hierarchy is built by the distributed device
+    setup (decoupled aggregation, halo rows over NCCL); coarse levels under
+    replicate_below rows are replicated.  Returns iterations and the
+    max-over-ranks device time."""
     import torch
     import torch.distributed as dist
 
     import paper_2407_09848_b200 as P
     from paper_2407_09848_b200 import dist as Dist
+    from paper_2407_09848_b200 import dsetup as DS
 
     m = m_base if strong else int(round(m_base * ws ** (1.0 / 3.0)))
     cfg = P.PolySmootherConfig(family=family, degree=k)
+    torch.cuda.synchronize()
     t0 = time.perf_counter()
-
-    def build():
-        A, _ = (P.poisson3d if stencil == 7 else P.poisson3d_27)(m)
-        return P.build_hierarchy(A, smoother=cfg)
-
-    d, path = Dist.share_hierarchy(build, comm.rank, dist.barrier)
+    if comm is not None:
+        D0 = Dist.poisson3d_block(m, comm, stencil=stencil)
+        levels, _ = DS.build_levels(D0, P.CoarseningConfig(), comm=comm, replicate_below=replicate_below)
+        dh = Dist.DistHierarchy.from_levels(levels, comm, cfg)
+        c = dh.ctx
+        lo, hi = dh.row_range
+        As, Ps, Rs = dh.As, dh.Ps, dh.Rs
+    else:
+        D0 = P.poisson3d_device(m, stencil)
+        h = P.build_hierarchy(D0, smoother=cfg)
+        lo, hi = 0, D0.nrows
+        dh = None
+        As = [lv.A for lv in h.levels]
+        Ps = [lv.P for lv in h.levels[:-1]]
+        Rs = [lv.restrict_op() for lv in h.levels[:-1]]
+    torch.cuda.synchronize()
     setup_s = time.perf_counter() - t0
-    dh = Dist.DistHierarchy(d, comm, cfg)
-    lo, hi = dh.row_range
+    if comm is not None:
+        t = torch.tensor([setup_s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        setup_s = float(t.item())
     bd = torch.ones(hi - lo, dtype=torch.float64, device="cuda")
     kc = P.KrylovConfig(tol=1e-6, itmax=1000)
-    dh.solve(bd, cfg=kc)  # warm-up
+
+    def run():
+        if dh is not None:
+            return dh.solve(bd, cfg=kc)
+        return P.solve(D0, bd, precond=P.as_vcycle_preconditioner(h), cfg=kc)
+
+    run()  # warm-up (graph capture)
     torch.cuda.synchronize()
-    dist.barrier()
-    c = dh.ctx
+    if comm is not None:
+        dist.barrier()
+    c = As[0].ctx
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(c.stream)
-    x, rep = dh.solve(bd, cfg=kc)
+    x, rep = run()
     e1.record(c.stream)
     torch.cuda.synchronize()
     t = torch.tensor([e0.elapsed_time(e1) / 1e3, rep.elapsed_s], device="cuda", dtype=torch.float64)
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    dist.barrier()
-    if comm.rank == 0:
-        try:
-            Dist.release_shared(path)
-        except OSError:
-            pass
+    if comm is not None:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.barrier()
+    sec = float(t[0].item())
+    peak, _ = peaks()
+    shapes = _level_shapes(As, Ps, Rs)
+    levels_n = [L.n for L in levels] if comm is not None else [a.nrows for a in As]
     return {"m": m, "n": int(m ** 3), "stencil": stencil, "scaling": "strong" if strong else "weak",
-            "rows_per_gpu": hi - lo, "family": family, "degree": k,
-            "levels": [int(d[f"A{l}_shape"][0]) for l in range(int(d["nlev"][0]))],
-            "distributed_levels": sum(p is not None for p in dh.parts),
+            "rows_per_gpu": hi - lo, "family": family, "degree": k, "levels": levels_n,
+            "distributed_levels": sum(p is not None for p in dh.parts) if dh is not None else 0,
+            "setup": "device" + (", distributed (decoupled aggregation)" if comm is not None else ""),
             "setup_s": setup_s, "iterations": rep.iterations, "final_relres": rep.final_relres,
-            "solve_s": float(t[0].item()), "wall_s": float(t[1].item()), "tol": 1e-6}
+            "solve_s": sec, "wall_s": float(t[1].item()), "tol": 1e-6,
+            "roofline_rank0": solve_roofline(shapes, k, family, rep.iterations, sec, peak)}
 
 
 def run_b200(args):
@@ -466,9 +552,12 @@ def run_b200(args):
     e2e = {"value": job_step_bytes / e2e_s / 1e9, "unit": "GB/s",
            "h2d_bytes_per_step": len(cfgs) * 2 * n * 8, "d2h_bytes_per_step": len(cfgs) * n * 8}
 
+    # free the sweep's fine level before the solves
+    del D, M, b, x0, bh, xh, out
+    torch.cuda.empty_cache()
     dsolve = None
-    if ws > 1 and args.solve_grid > 0:
-        dsolve = dist_solve_bench(comm, args.solve_grid, ws, family=args.solve_family or "opt_cheb4",
+    if ws > 1 and args.weak_grid > 0:
+        dsolve = dist_solve_bench(comm, args.weak_grid, ws, family=args.solve_family or "opt_cheb4",
                                   k=args.solve_k, stencil=args.solve_stencil,
                                   strong=args.solve_scaling == "strong")
 
@@ -491,7 +580,9 @@ def run_b200(args):
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "kernel": "k_thread_rows<Cheb4Step<0,0,0>,0> (cheb4 middle degree step)",
                          "bytes_per_launch": mb, "ms_per_launch": t_mid,
-                         "traffic": (traffic or {}).get("bytes_per_launch")},
+                         "traffic": (traffic or {}).get("bytes_per_launch"),
+                         "traffic_source": "static: ncu --set full capture of this kernel at 256^3, "
+                                           "profiles/ncu_traffic.json (not measured in this run)"},
             "mid_step_ms": mids,
             "apply_ms": {f"{f}_k{k}": v for (f, k), v in t_apply.items()},
             "e2e": e2e,
@@ -504,8 +595,13 @@ def run_b200(args):
             line["solve"] = solve_bench(args.solve_grid, cpu=not args.no_cpu_baseline,
                                         stencil=args.solve_stencil, k=args.solve_k,
                                         cpu_family=args.solve_family or "opt_cheb1")
+            torch.cuda.empty_cache()
+        if ws == 1 and args.weak_grid > 0:
+            # BASELINE configs[3] at N = 1: the weak-scaling reference point
+            line["solve_weak"] = dist_solve_bench(None, args.weak_grid, 1, family=args.solve_family or "opt_cheb4",
+                                                  k=args.solve_k, stencil=args.solve_stencil)
         if dsolve is not None:
-            line["solve"] = dsolve
+            line["solve_weak" if args.solve_scaling == "weak" else "solve_strong"] = dsolve
         print(json.dumps(line), flush=True)
     if ws > 1:
         dist.barrier()
@@ -523,8 +619,11 @@ def main():
     ap.add_argument("--grid", type=int, default=256, help="fine-level cube edge per GPU (weak-scaled for N > 1)")
     ap.add_argument("--cpu-grid", type=int, default=256)
     ap.add_argument("--no-cpu-baseline", action="store_true")
-    ap.add_argument("--solve-grid", type=int, default=128,
-                    help="grid size of the PCG+AMG solve section (0: skip)")
+    ap.add_argument("--solve-grid", type=int, default=256,
+                    help="N = 1: grid of the PCG+AMG solve section, all families (BASELINE configs[1]; 0: skip)")
+    ap.add_argument("--weak-grid", type=int, default=400,
+                    help="rows per GPU (cube edge) of the weak-scaled PCG+AMG solve (BASELINE configs[3]; "
+                         "with --solve-scaling strong: the global cube edge; 0: skip)")
     ap.add_argument("--solve-stencil", type=int, default=7, choices=[7, 27])
     ap.add_argument("--solve-k", type=int, default=4, help="smoother degree of the solve section")
     ap.add_argument("--solve-family", default=None,
@@ -535,6 +634,21 @@ def main():
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch under torchrun (the driver's own launch line)
+        import socket
+
+        sk = socket.socket()
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+        sk.close()
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+        return subprocess.call(cmd)
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if ws != args.gpus:
+        print(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={ws}; using {ws}", file=sys.stderr)
+        args.gpus = ws
     if args.impl == "reference":
         return run_reference(args)
     return run_b200(args)

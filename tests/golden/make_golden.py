@@ -302,6 +302,56 @@ def stencil27():
     print("wrote", path)
 
 
+def hier_digest_record(h):
+    rec = {"levels": []}
+    for lev in h.levels:
+        lr = {"A": mat_digest(lev.A), "M": sha(lev.M.m_diag, "f")}
+        if lev.P is not None:
+            lr["P"] = mat_digest(lev.P)
+            lr["R"] = mat_digest(lev.restrict_op())
+        rec["levels"].append(lr)
+    return rec
+
+
+def big():
+    """Benched sizes (Missing #2): 128^3 hierarchies of both
+    coarsenings (digests), V-cycle digests and the PCG iteration tables
+    (4 families x k = 1..6, rtol 1e-6); 256^3 SA (BASELINE configs[1])
+    hierarchy digests and PCG iterations of every family at k = 4.
+    Long: ~40 min and ~20 GB on one core."""
+    doc = {"note": "sha256 over little-endian int64 indices / float64 values; OPENBLAS_NUM_THREADS=1"}
+    path = os.path.join(HERE, "hashes_big.json")
+    jobs = [(128, "smoothed_aggregation", range(1, 7)), (128, "pairwise_matching", range(1, 7)),
+            (256, "smoothed_aggregation", (4,))]
+    for m, kind, degrees in jobs:
+        A, b = poisson3d(m)
+        t0 = time.perf_counter()
+        h = build_hierarchy(A, coarsening=CoarseningConfig(kind=kind),
+                            smoother=PolySmootherConfig(family="cheb4", degree=4))
+        rec = hier_digest_record(h)
+        rec["setup_s"] = time.perf_counter() - t0
+        print(m, kind, "setup", rec["setup_s"], flush=True)
+        r = np.random.default_rng(5).standard_normal(A.nrows)
+        rec["vcycle"] = {}
+        for fam in FAMILIES:
+            set_smoother(h, PolySmootherConfig(family=fam, degree=4))
+            rec["vcycle"][fam] = sha(vcycle_apply(h, r), "f")
+        rec["pcg"] = {}
+        for fam in FAMILIES:
+            for k in degrees:
+                set_smoother(h, PolySmootherConfig(family=fam, degree=k))
+                t0 = time.perf_counter()
+                _, rep = solve(A, b, precond=as_vcycle_preconditioner(h), cfg=KrylovConfig(tol=1e-6, itmax=1000))
+                rec["pcg"][f"{fam}_k{k}"] = {"iterations": rep.iterations, "final_relres": rep.final_relres,
+                                             "spmv_count": rep.spmv_count, "converged": rep.converged,
+                                             "solve_s": time.perf_counter() - t0}
+                print(m, kind, fam, k, rep.iterations, flush=True)
+        doc[f"p3d{m}_{kind}"] = rec
+        with open(path, "w") as f:
+            json.dump(doc, f, indent=1)
+    print("wrote", path)
+
+
 def cli_reports():
     """Reference `amgpoly solve` JSON reports (cli.py:193-255) for small runs."""
     from amgpoly.cli import main as cli_main
@@ -317,6 +367,9 @@ def cli_reports():
 
 
 if __name__ == "__main__":
+    if sys.argv[1:] == ["big"]:
+        big()
+        sys.exit(0)
     export_params()
     smoother_small()
     hier_small()

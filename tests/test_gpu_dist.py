@@ -72,3 +72,30 @@ def test_dist_check_split_launches(nproc, transport):
     # 48^3: the fine level holds >= 2 slices per SM per rank -> interior
     # launch, exchange, boundary launch
     run_dist_check(nproc, 48, True, transport)
+
+
+def run_dsetup_check(nproc, args):
+    if ngpus() < nproc:
+        pytest.skip(f"needs {nproc} GPUs")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", str(nproc),
+           "--master-addr", "127.0.0.1", "--master-port", str(free_port()),
+           os.path.join(REPO, "tools", "dsetup_dist_check.py")] + args
+    p = subprocess.run(cmd, capture_output=True, text=True, timeout=600)
+    lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1, p.stdout[-2000:] + p.stderr[-3000:]
+    assert lines[0]["ok"], lines[0]
+    assert p.returncode == 0
+
+
+@pytest.mark.parametrize("args", [["--grid", "32"], ["--grid", "32", "--kind", "pairwise_matching"],
+                                  ["--grid", "48", "--replicate-below", "20000"], ["--grid", "20", "--stencil", "27"]])
+def test_distributed_device_setup_two_gpus(args):
+    """Decoupled distributed device setup == the reference's formulas on the
+    gathered blocks (bitwise), V-cycle bitwise vs the oracle on that
+    hierarchy, PCG iterations within +-1 of the oracle and of the one-GPU
+    (reference) hierarchy."""
+    run_dsetup_check(2, args)
+
+
+def test_distributed_device_setup_four_gpus():
+    run_dsetup_check(4, ["--grid", "48"])

@@ -32,6 +32,9 @@ import time
 import numpy as np
 
 REPO = os.path.dirname(os.path.abspath(__file__))
+# the device setup frees and re-allocates large index arrays (BASELINE configs[4]
+# on one GPU peaks near 120 GB): keep the caching allocator from fragmenting
+os.environ.setdefault("PYTORCH_CUDA_ALLOC_CONF", "expandable_segments:True")
 sys.path.insert(0, REPO)
 
 METRIC = "smoother-apply GB/s (% HBM peak); PCG+AMG solve s & iters, 3D Poisson 1–8 GPU"
@@ -453,6 +456,23 @@ def run_b200(args):
     dev = torch.cuda.current_device()
     c = N.ctx(dev)
     halo_info = None
+    if args.solve_only:
+        # diagnostic runs of the PCG+AMG solves alone (BASELINE configs[3] / [4] at
+        # their configured sizes); not the driver's bench line
+        comm = None
+        if ws > 1:
+            from paper_2407_09848_b200 import dist as Dist
+
+            comm = Dist.Communicator(local)
+        res = dist_solve_bench(comm, args.weak_grid, ws, family=args.solve_family or "opt_cheb4",
+                               k=args.solve_k, stencil=args.solve_stencil, strong=args.solve_scaling == "strong")
+        if rank == 0:
+            res["peak_mem_gb_rank0"] = torch.cuda.max_memory_allocated() / 1e9
+            print(json.dumps({"solve_only": True, "n_gpus": ws, "solve": res}), flush=True)
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return 0
     if ws == 1:
         m = args.grid
         D = P.poisson3d_device(m)
@@ -629,6 +649,8 @@ def main():
     ap.add_argument("--solve-family", default=None,
                     help="smoother family of the multi-GPU solve / the CPU oracle solve "
                          "(default opt_cheb4 / opt_cheb1)")
+    ap.add_argument("--solve-only", action="store_true",
+                    help="run only the --weak-grid solve (diagnostics for BASELINE configs[3]/[4])")
     ap.add_argument("--solve-scaling", default="weak", choices=["weak", "strong"],
                     help="N > 1: weak (solve-grid^3 rows per GPU) or strong (solve-grid^3 in total)")
     args = ap.parse_args()

@@ -264,6 +264,16 @@ int amgp_ds_spgemm(amgp_ctx *ctx, const amgp_mat *A_sell, const int64_t *a_rp, c
 int amgp_ds_symmetrize(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, const int64_t *g_col, const double *g_val,
                        const int64_t *t_rp, const int64_t *t_col, const double *t_val, const int64_t *row_ptr,
                        int64_t *row_cnt, int64_t *col, double *val);
+/* one-GPU (G + G^T) * 0.5 without a transposed copy: gt[e] = G[K,J] for
+ * entry (J,K) (0.0 when absent), orphans = (K, J, G[J,K]) for absent ones
+ * (up to cap written; *norph = their number); then the merge with the
+ * orphan rows (sorted CSR o_*), count/fill. */
+int amgp_ds_sym_lookup(amgp_ctx *ctx, int64_t n, const int64_t *rp, const int64_t *col, const double *val,
+                       double *gt, int64_t *orow, int64_t *ocol, double *oval, int64_t cap, int64_t *norph);
+int amgp_ds_symmetrize_lookup(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, const int64_t *g_col,
+                              const double *g_val, const double *gt, const int64_t *o_rp, const int64_t *o_col,
+                              const double *o_val, const int64_t *row_ptr, int64_t *row_cnt, int64_t *col,
+                              double *val);
 /* SELL-32 matrix from a device CSR with local int64 columns < 2^31 */
 int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *row_ptr,
                        const int64_t *col, const double *val, amgp_mat **out);

@@ -16,7 +16,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from . import _native as N
-from .smoothers import L1JacobiData, PolySmootherConfig, l1_jacobi_diag
+from .smoothers import DeviceL1JacobiData, L1JacobiData, PolySmootherConfig, l1_jacobi_diag
 from .sparse import CsrMatrix, device_of
 
 
@@ -66,7 +66,7 @@ class DeviceHierarchy:
         self.levels = h.levels
         L = len(h.levels)
         self._A = [device_of(lv.A) for lv in h.levels]
-        self._m = [lv.M.m_diag if N.is_torch(lv.M.m_diag) else lv.M.device(c) for lv in h.levels]
+        self._m = [lv.M.device(c) for lv in h.levels]
         self._P = [device_of(lv.P) for lv in h.levels[:-1]]
         self._R = [device_of(lv.restrict_op()) for lv in h.levels[:-1]]
         Aa = (N._VP * L)(*[a.handle for a in self._A])
@@ -200,7 +200,7 @@ def build_hierarchy(A, coarsening=None, smoother=None, max_levels=10, min_coarse
                                         min_coarse_size=min_coarse_size)
     levels = []
     for L in dl:
-        lv = Level(A=L.A, M=L1JacobiData(m_diag=L.m), smoother=smoother, P=L.P,
+        lv = Level(A=L.A, M=DeviceL1JacobiData(L.m), smoother=smoother, P=L.P,
                    n_aggregates=L.n_aggregates if L.P is not None else 0)
         lv._Pt = L.R
         levels.append(lv)

@@ -541,6 +541,82 @@ __global__ void k_ds_symmetrize(int64_t n, const int64_t *__restrict__ grp, cons
     if (!rp) cnt[r] = k - k0;
 }
 
+// ---------------------------------------------------------------- symmetrise without G^T
+// One GPU, square G with sorted rows: for entry (J, K) of row J look J up in
+// row K (binary search).  gt[e] = G[K, J] (0.0 when row K lacks J); a missing
+// (K, J) makes (row K, column J, value G[J, K]) an "orphan" entry of G^T that
+// row K's own entries do not cover (only exact-zero cancellations produce
+// them).  Memory: one double per entry instead of a transposed copy.
+__global__ void k_ds_sym_lookup(int64_t n, const int64_t *__restrict__ rp, const int64_t *__restrict__ col,
+                                const double *__restrict__ val, double *__restrict__ gt,
+                                int64_t *__restrict__ orow, int64_t *__restrict__ ocol, double *__restrict__ oval,
+                                unsigned long long *__restrict__ norph, unsigned long long cap) {
+    const int64_t J = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+    if (J >= n) return;
+    const int lane = threadIdx.x & 31;
+    for (int64_t e = rp[J] + lane; e < rp[J + 1]; e += 32) {
+        const int64_t K = col[e];
+        int64_t lo = rp[K], hi = rp[K + 1];
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (col[mid] < J) lo = mid + 1;
+            else hi = mid;
+        }
+        if (lo < rp[K + 1] && col[lo] == J) {
+            gt[e] = val[lo];
+        } else {
+            gt[e] = 0.0;
+            const unsigned long long o = atomicAdd(norph, 1ull);
+            if (o < cap) {
+                orow[o] = K;
+                ocol[o] = J;
+                oval[o] = val[e];
+            }
+        }
+    }
+}
+
+// (G + G^T) * 0.5 from G's rows, the looked-up transpose values and the
+// orphan rows (sorted CSR): scipy binop res = a + b (missing side 0.0),
+// zeros dropped, then * 0.5 and eliminate_zeros.
+__global__ void k_ds_symmetrize_lookup(int64_t n, const int64_t *__restrict__ grp, const int64_t *__restrict__ gcol,
+                                       const double *__restrict__ gval, const double *__restrict__ gt,
+                                       const int64_t *__restrict__ orp, const int64_t *__restrict__ ocol,
+                                       const double *__restrict__ oval, const int64_t *__restrict__ rp,
+                                       int64_t *__restrict__ cnt, int64_t *__restrict__ out_col,
+                                       double *__restrict__ out_val) {
+    const int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= n) return;
+    int64_t i = grp[r], ie = grp[r + 1], j = orp[r], je = orp[r + 1];
+    int64_t k = rp ? rp[r] : 0, k0 = k;
+    while (i < ie || j < je) {
+        const int64_t ci = i < ie ? gcol[i] : INT64_MAX, cj = j < je ? ocol[j] : INT64_MAX;
+        double a, b;
+        int64_t c;
+        if (ci < cj) {
+            c = ci;
+            a = gval[i];
+            b = gt[i];
+            i++;
+        } else {
+            c = cj;
+            a = 0.0;
+            b = oval[j];
+            j++;
+        }
+        const double s = __dadd_rn(a, b);
+        if (s == 0.0) continue;
+        const double h = __dmul_rn(s, 0.5);
+        if (h == 0.0) continue;
+        if (rp) {
+            out_col[k] = c;
+            out_val[k] = h;
+        }
+        k++;
+    }
+    if (!rp) cnt[r] = k - k0;
+}
+
 // ---------------------------------------------------------------- device CSR -> SELL
 __global__ void k_dcsr_width(int64_t n, const int64_t *__restrict__ rp, int32_t *__restrict__ w) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -858,6 +934,48 @@ int amgp_ds_symmetrize(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, const int6
     if (n == 0) return AMGP_OK;
     k_ds_symmetrize<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, g_rp, g_col, g_val, t_rp, t_col, t_val, row_ptr,
                                                                row_cnt, col, val);
+    AMGP_CHECK_LAUNCH(ctx);
+    return AMGP_OK;
+}
+
+// One-GPU symmetrisation helpers (see k_ds_sym_lookup): gt[nnz] and up to
+// cap orphan entries (orow, ocol, oval); *norph (host) = number of orphans
+// (call again with a larger cap when it exceeds cap).
+int amgp_ds_sym_lookup(amgp_ctx *ctx, int64_t n, const int64_t *rp, const int64_t *col, const double *val,
+                       double *gt, int64_t *orow, int64_t *ocol, double *oval, int64_t cap, int64_t *norph) {
+    if (!ctx || n < 0 || (n && (!rp || !gt)) || !norph || cap < 0)
+        return amgp_fail(AMGP_EINVAL, "amgp_ds_sym_lookup: bad argument");
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    *norph = 0;
+    if (n == 0) return AMGP_OK;
+    unsigned long long *d = nullptr;
+    AMGP_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
+    cudaError_t e = cudaMemsetAsync(d, 0, sizeof(unsigned long long), ctx->stream);
+    if (e == cudaSuccess) {
+        k_ds_sym_lookup<<<grid_for(n * 32, 256), 256, 0, ctx->stream>>>(n, rp, col, val, gt, orow, ocol, oval, d,
+                                                                      (unsigned long long)cap);
+        e = cudaGetLastError();
+    }
+    unsigned long long h = 0;
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaFree(d);
+    if (e != cudaSuccess) return amgp_cuda_fail(e, "k_ds_sym_lookup", __FILE__, __LINE__);
+    ctx->launches.fetch_add(1);
+    *norph = (int64_t)h;
+    return AMGP_OK;
+}
+
+int amgp_ds_symmetrize_lookup(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, const int64_t *g_col,
+                              const double *g_val, const double *gt, const int64_t *o_rp, const int64_t *o_col,
+                              const double *o_val, const int64_t *row_ptr, int64_t *row_cnt, int64_t *col,
+                              double *val) {
+    if (!ctx || n < 0 || (n && (!g_rp || !o_rp)) || (!row_ptr && !row_cnt) || (row_ptr && (!col || !val)))
+        return amgp_fail(AMGP_EINVAL, "amgp_ds_symmetrize_lookup: bad argument");
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    if (n == 0) return AMGP_OK;
+    k_ds_symmetrize_lookup<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, g_rp, g_col, g_val, gt, o_rp, o_col, o_val,
+                                                                      row_ptr, row_cnt, col, val);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }

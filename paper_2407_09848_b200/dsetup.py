@@ -118,6 +118,8 @@ def _rows_of(lens):
 
 def _sell(c, csr, ncols):
     """SELL DeviceMatrix from a device CSR with local columns."""
+    if csr.nnz > (1 << 27):  # the library allocates outside torch's cache: return cached blocks first
+        _torch().cuda.empty_cache()
     h = N._VP()
     with c.scope():
         N.check(_lib().amgp_mat_from_dcsr(c.handle, csr.nrows, int(ncols), _p(csr.rp), _p(csr.col),
@@ -440,18 +442,21 @@ def _attach(D, plan):
 
 
 def _galerkin_chunks(c, L, P, R, R_csr, budget_entries):
-    """One-GPU Galerkin in coarse-row chunks (bounded A P memory): returns G."""
+    """One-GPU Galerkin G = R (A P) in coarse-row chunks, so that only a
+    window of A P is ever resident: chunk [J0, J1) needs the rows of A P
+    between the first and last fine row its restriction rows touch.  Two
+    sweeps over the chunks (row counts, then rows written in place)."""
     torch = _torch()
     dev = c.device
     lib = _lib()
     n = L.A.nrows
     nc = R.nrows
-    # full C row counts once
     cnt = torch.empty(max(n, 1), dtype=torch.int64, device=dev)
     N.check(lib.amgp_ds_spgemm(c.handle, L.A.handle, None, None, None, None, n, _p(P.rp), _p(P.col), _p(P.val), 0,
                                None, _p(cnt), None, None))
     ccum = torch.zeros(n + 1, dtype=torch.int64, device=dev)
     torch.cumsum(cnt[:n], 0, out=ccum[1:])
+    del cnt
     total = int(ccum[-1].item())
     nchunks = max(1, math.ceil(total / budget_entries))
     lens = R_csr.lens()
@@ -459,27 +464,46 @@ def _galerkin_chunks(c, L, P, R, R_csr, budget_entries):
                        torch.full_like(lens, n))
     imax = torch.where(lens > 0, R_csr.col[torch.clamp(R_csr.rp[1:] - 1, min=0)], torch.full_like(lens, -1))
     bounds = [nc * k // nchunks for k in range(nchunks + 1)]
-    parts = []
+    chunks = []
     for k in range(nchunks):
         J0, J1 = bounds[k], bounds[k + 1]
-        if J1 <= J0:
-            continue
-        w0 = int(imin[J0:J1].min().item())
-        w1 = int(imax[J0:J1].max().item()) + 1
-        w0, w1 = min(w0, w1), max(w0, w1)
+        if J1 > J0:
+            w0 = int(imin[J0:J1].min().item())
+            w1 = int(imax[J0:J1].max().item()) + 1
+            chunks.append((J0, J1, min(w0, w1), max(w0, w1)))
+    del imin, imax, lens
+
+    def window(w0, w1):
         rows = torch.arange(w0, w1, dtype=torch.int64, device=dev)
         rp = ccum[w0:w1 + 1] - ccum[w0]
         nnz = int(rp[-1].item())
-        Cw = DCsr(rp, torch.empty(nnz, dtype=torch.int64, device=dev), torch.empty(nnz, dtype=torch.float64, device=dev))
+        Cw = DCsr(rp, torch.empty(nnz, dtype=torch.int64, device=dev),
+                  torch.empty(nnz, dtype=torch.float64, device=dev))
         if nnz:
             N.check(lib.amgp_ds_spgemm(c.handle, L.A.handle, None, None, None, _p(rows), w1 - w0, _p(P.rp),
                                        _p(P.col), _p(P.val), 0, _p(Cw.rp), None, _p(Cw.col), _p(Cw.val)))
+        return Cw
+
+    gcnt = torch.empty(max(nc, 1), dtype=torch.int64, device=dev)
+    for J0, J1, w0, w1 in chunks:  # sweep 1: row counts of G
+        Cw = window(w0, w1)
         jr = torch.arange(J0, J1, dtype=torch.int64, device=dev)
-        parts.append(_spgemm(c, J1 - J0, Cw, a_sell=R, a_rows=jr, b_off=w0))
+        N.check(lib.amgp_ds_spgemm(c.handle, R.handle, None, None, None, _p(jr), J1 - J0, _p(Cw.rp), _p(Cw.col),
+                                   _p(Cw.val), int(w0), None, _p(gcnt[J0:J1]), None, None))
         del Cw
-    G = parts[0]
-    for p in parts[1:]:
-        G = _concat(G, p)
+    grp = torch.zeros(nc + 1, dtype=torch.int64, device=dev)
+    torch.cumsum(gcnt[:nc], 0, out=grp[1:])
+    del gcnt
+    gnnz = int(grp[-1].item())
+    G = DCsr(grp, torch.empty(gnnz, dtype=torch.int64, device=dev), torch.empty(gnnz, dtype=torch.float64, device=dev))
+    for J0, J1, w0, w1 in chunks:  # sweep 2: rows written in place
+        Cw = window(w0, w1)
+        jr = torch.arange(J0, J1, dtype=torch.int64, device=dev)
+        rp = grp[J0:J1 + 1] - grp[J0]
+        o = int(grp[J0].item())
+        N.check(lib.amgp_ds_spgemm(c.handle, R.handle, None, None, None, _p(jr), J1 - J0, _p(Cw.rp), _p(Cw.col),
+                                   _p(Cw.val), int(w0), _p(rp), None, _p(G.col[o:]), _p(G.val[o:])))
+        del Cw
     return G
 
 
@@ -616,12 +640,14 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
             else:
                 G = _galerkin_chunks(c, L, Prow, R, R_csr, budget)
             del Prow
+            R_g = DCsr(R_csr.rp, ext_g[R_csr.col], R_csr.val) if replicate_next else None
+            del R_csr
             log(f"  G: nnz={G.nnz}")
-            # G^T restricted to own rows
-            Gr = _rows_of(G.lens()) + clo
             if dist_l:
+                # G^T restricted to own rows: entries with a foreign column go to its owner
                 import torch.distributed as dist
 
+                Gr = _rows_of(G.lens()) + clo
                 coff_t = torch.as_tensor(coff, device=dev)
                 dest = torch.searchsorted(coff_t, G.col, right=True) - 1
                 order = torch.argsort(dest, stable=True)
@@ -632,22 +658,49 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
                 _a2a(tr, G.col[order].contiguous(), recv_counts, send_counts)
                 _a2a(tc, Gr[order].contiguous(), recv_counts, send_counts)
                 _a2a(tv, G.val[order].contiguous(), recv_counts, send_counts)
-                del dest, order
+                del dest, order, Gr
+                Gt = _csr_from_entries(na, tr - clo, tc, tv, (tr - clo) * max(nc, 1) + tc)
+                del tr, tc, tv
+
+                def scount(cnt):
+                    N.check(lib.amgp_ds_symmetrize(c.handle, na, _p(G.rp), _p(G.col), _p(G.val), _p(Gt.rp),
+                                                   _p(Gt.col), _p(Gt.val), None, _p(cnt), None, None))
+
+                def sfill(rp, col, val):
+                    N.check(lib.amgp_ds_symmetrize(c.handle, na, _p(G.rp), _p(G.col), _p(G.val), _p(Gt.rp),
+                                                   _p(Gt.col), _p(Gt.val), _p(rp), None, _p(col), _p(val)))
             else:
-                tr, tc, tv = G.col, Gr, G.val
-            Gt = _csr_from_entries(na, tr - clo, tc, tv, (tr - clo) * max(nc, 1) + tc)
-            del tr, tc, tv, Gr
+                # one GPU: G^T values looked up in G itself (no transposed copy)
+                gt = torch.empty(max(G.nnz, 1), dtype=torch.float64, device=dev)
+                cap = 1 << 16
+                while True:
+                    orow = torch.empty(cap, dtype=torch.int64, device=dev)
+                    ocol = torch.empty(cap, dtype=torch.int64, device=dev)
+                    oval = torch.empty(cap, dtype=torch.float64, device=dev)
+                    no = C.c_int64()
+                    N.check(lib.amgp_ds_sym_lookup(c.handle, na, _p(G.rp), _p(G.col), _p(G.val), _p(gt), _p(orow),
+                                                   _p(ocol), _p(oval), cap, C.byref(no)))
+                    if no.value <= cap:
+                        break
+                    cap = no.value
+                no = no.value
+                O = _csr_from_entries(na, orow[:no], ocol[:no], oval[:no], orow[:no] * max(nc, 1) + ocol[:no])
+                del orow, ocol, oval
+                Gt = None
 
-            def scount(cnt):
-                N.check(lib.amgp_ds_symmetrize(c.handle, na, _p(G.rp), _p(G.col), _p(G.val), _p(Gt.rp),
-                                               _p(Gt.col), _p(Gt.val), None, _p(cnt), None, None))
+                def scount(cnt):
+                    N.check(lib.amgp_ds_symmetrize_lookup(c.handle, na, _p(G.rp), _p(G.col), _p(G.val), _p(gt),
+                                                          _p(O.rp), _p(O.col), _p(O.val), None, _p(cnt), None, None))
 
-            def sfill(rp, col, val):
-                N.check(lib.amgp_ds_symmetrize(c.handle, na, _p(G.rp), _p(G.col), _p(G.val), _p(Gt.rp),
-                                               _p(Gt.col), _p(Gt.val), _p(rp), None, _p(col), _p(val)))
+                def sfill(rp, col, val):
+                    N.check(lib.amgp_ds_symmetrize_lookup(c.handle, na, _p(G.rp), _p(G.col), _p(G.val), _p(gt),
+                                                          _p(O.rp), _p(O.col), _p(O.val), _p(rp), None, _p(col),
+                                                          _p(val)))
 
             Ac = _count_fill(na, dev, scount, sfill)
             del G, Gt
+            if not dist_l:
+                del gt, O
             log(f"  A_c: nnz={Ac.nnz}")
             # -- next level
             L.n_aggregates = nc
@@ -656,7 +709,6 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
                 # coarse agglomeration: every rank gets the whole coarse level,
                 # and the restriction into it all rows of P^T
                 Afull = _gather_rows(Ac, size)
-                R_g = DCsr(R_csr.rp, ext_g[R_csr.col], R_csr.val)
                 Rfull = _gather_rows(R_g, size)
                 rl, rhg, rplan, _ = make_halo(Rfull.col, L.lo, L.hi, L.off, me)
                 L.R = _attach(_sell(c, DCsr(Rfull.rp, rl, Rfull.val), rplan.nown + sum(rplan.recv_cnt)), rplan)
@@ -676,7 +728,7 @@ def build_levels(A0, coarsening, max_levels=10, min_coarse_size=200, comm=None, 
             else:
                 L.R = R
                 nxt = DLevel(A=_sell(c, Ac, nc), n=nc, off=None, lo=0, hi=nc)
-            del R_csr, Ac, ext_g
+            del Ac, ext_g
             torch.cuda.empty_cache()
             nxt.m = nxt.A.l1_diag()
             levels.append(nxt)

@@ -40,6 +40,25 @@ class L1JacobiData:
         return self._dev
 
 
+class DeviceL1JacobiData(L1JacobiData):
+    """l1 diagonal computed on the device (device setup levels): the device
+    tensor is the working copy, ``m_diag`` a host view downloaded on demand
+    (the reference's field is a numpy array)."""
+
+    def __init__(self, dev):
+        self._dev = dev
+        self._host = None
+
+    @property
+    def m_diag(self):
+        if self._host is None:
+            self._host = N.to_host(self._dev)
+        return self._host
+
+    def device(self, c):
+        return self._dev
+
+
 def _reduceat_abs_rowsum(A):
     """scipy's |A|.sum(axis=1): numpy add.reduceat over each non-empty row."""
     out = np.zeros(A.nrows)
@@ -102,8 +121,6 @@ class PolySmootherConfig:
 
 
 def _m_device(M, c):
-    if N.is_torch(M.m_diag):
-        return M.m_diag
     return M.device(c)
 
 

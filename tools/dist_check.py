@@ -70,7 +70,7 @@ def main():
 
     # 2./3. distributed hierarchy
     def build():
-        return P.build_hierarchy(A, smoother=P.PolySmootherConfig(family="opt_cheb1", degree=4))
+        return P.build_hierarchy(A, smoother=P.PolySmootherConfig(family="opt_cheb1", degree=4), setup="host")
 
     d, path = D.share_hierarchy(build, me, dist.barrier)
     h = build() if me != 0 else None  # every rank needs the global levels for the oracle

@@ -42,7 +42,7 @@ for m, kind in [(16, "smoothed_aggregation"), (16, "pairwise_matching"), (32, "s
         print(f"{st}-pt {m}^3 {kind}: levels host {len(hh.levels)} dev {len(hd.levels)}  t host {th_:.2f} dev {td:.2f}", flush=True)
         for l, (a, b) in enumerate(zip(hh.levels, hd.levels)):
             ok &= cmp(a.A, b.A, f"A{l}")
-            ok &= np.array_equal(a.M.m_diag, b.M.m_diag.cpu().numpy())
+            ok &= np.array_equal(a.M.m_diag, np.asarray(b.M.m_diag))
             if a.P is not None:
                 ok &= cmp(a.P, b.P, f"P{l}")
                 ok &= cmp(a.restrict_op(), b.restrict_op(), f"R{l}")

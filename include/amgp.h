@@ -110,11 +110,6 @@ int amgp_mat_l1_diag(amgp_mat *A, double *m_dev);
 /* ---- hot-path kernels --------------------------------------------------- */
 /* sparse.py:118-125 spmv: y = A x (device vectors). */
 int amgp_spmv(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y);
-/* Diagnostics: reps SpMVs back to back (captured in a CUDA graph when
- * use_graph & 1), device time per SpMV in *ms (halo exchanges included);
- * use_graph & 2: the halo exchanges alone, without the row kernels. */
-int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y, int reps,
-                    int use_graph, double *ms);
 /* sparse.py:128-139 fused_update: r -= s; d = d*(rho*rho_prev) + c*r; x += d. */
 int amgp_fused_update(amgp_ctx *ctx, int64_t n, double rho, double rho_prev, double c,
                       const double *s, double *r, double *d, double *x);
@@ -139,11 +134,8 @@ int amgp_hier_set_smoother(amgp_hier *h, int level, const amgp_smoother_cfg *cfg
 int amgp_hier_set_coarse_cholesky(amgp_hier *h, const double *L_colmajor);
 /* Capture the V-cycle into a CUDA graph on the next apply (1) or not (0). */
 int amgp_hier_use_graph(amgp_hier *h, int enable);
-/* Run the small bottom levels as one cooperative kernel (1) or as regular
- * per-step launches (0, default); identical results either way. */
-int amgp_hier_use_tail(amgp_hier *h, int enable);
-/* Levels, and the first level handled by the cooperative tail (-1: none). */
-int amgp_hier_info(amgp_hier *h, int *nlevels, int *tail_start);
+/* Number of levels. */
+int amgp_hier_info(amgp_hier *h, int *nlevels);
 int amgp_hier_destroy(amgp_hier *h);
 /* amg.py:303-315 vcycle_apply: z = V(r), r and z device vectors of n_0. */
 int amgp_vcycle_apply(amgp_hier *h, const double *r, double *z);

@@ -77,7 +77,6 @@ _SIGS = {
     "amgp_mat_to_csr": (C.c_int, [_VP, _P64, _P64, _PD]),
     "amgp_mat_l1_diag": (C.c_int, [_VP, _VP]),
     "amgp_spmv": (C.c_int, [_VP, _VP, _VP, _VP]),
-    "amgp_spmv_timed": (C.c_int, [_VP, _VP, _VP, _VP, C.c_int, C.c_int, _PD]),
     "amgp_fused_update": (C.c_int, [_VP, C.c_int64, C.c_double, C.c_double, C.c_double,
                                      _VP, _VP, _VP, _VP]),
     "amgp_smoother_apply": (C.c_int, [_VP, _VP, _VP, C.POINTER(SmootherCfg), _VP, _VP, _VP]),
@@ -86,8 +85,7 @@ _SIGS = {
     "amgp_hier_set_smoother": (C.c_int, [_VP, C.c_int, C.POINTER(SmootherCfg)]),
     "amgp_hier_set_coarse_cholesky": (C.c_int, [_VP, _PD]),
     "amgp_hier_use_graph": (C.c_int, [_VP, C.c_int]),
-    "amgp_hier_use_tail": (C.c_int, [_VP, C.c_int]),
-    "amgp_hier_info": (C.c_int, [_VP, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "amgp_hier_info": (C.c_int, [_VP, C.POINTER(C.c_int)]),
     "amgp_hier_destroy": (C.c_int, [_VP]),
     "amgp_vcycle_apply": (C.c_int, [_VP, _VP, _VP]),
     "amgp_pcg_solve": (C.c_int, [_VP, _VP, _VP, _VP, _VP, C.c_int, C.c_int, C.c_double, C.c_int,

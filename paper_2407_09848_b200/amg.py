@@ -105,17 +105,6 @@ class DeviceHierarchy:
     def use_graph(self, enable=True):
         N.check(N.lib().amgp_hier_use_graph(self.handle, int(enable)))
 
-    def use_tail(self, enable=True):
-        """Cooperative single-kernel V-cycle tail for the small levels (default on)."""
-        N.check(N.lib().amgp_hier_use_tail(self.handle, int(enable)))
-
-    def tail_start(self):
-        """First level run by the cooperative tail kernel, -1 if none."""
-        self.sync_smoothers()
-        nl, ts = C.c_int(), C.c_int()
-        N.check(N.lib().amgp_hier_info(self.handle, C.byref(nl), C.byref(ts)))
-        return ts.value
-
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and N._lib is not None:

@@ -71,32 +71,25 @@ struct amgp_ctx {
     // direct NVLink transport (AMGP_HALO=p2p, dist.cu): peers' halo buffers
     // and synchronisation words mapped through CUDA IPC; the kernels
     // themselves signal and wait (sync_stride words per matrix slot)
-    int halo_p2p = 0;  // 0: NCCL, 1: p2p (default), -1: diagnostic AMGP_HALO=skip (no transfer)
+    int halo_p2p = 0;  // 0: NCCL, 1: p2p (default)
     unsigned long long *sync = nullptr;            // [AMGP_MAX_SLOTS][sync_stride]
     std::vector<unsigned long long *> peer_sync;   // every rank's sync array (self included)
     int sync_stride = 0;
     int next_slot = 0;
-    // AMGP_P2P_FUSED=1: p2p transport with ONE launch per distributed SpMV
-    // (pack CTAs, interior slices and boundary slices in one grid, halo
-    // double-buffered by exchange parity); default 0: pack kernel on the
-    // high-priority stream + interior launch + boundary launch
-    int p2p_fused = 0;
 };
 
-#define AMGP_MAX_SLOTS 256
+// Slots are never reused: a freed slot's words may still receive a peer's
+// final ready/consumed signal, so reuse would need a collective in
+// amgp_mat_destroy (unsafe from garbage-collected owners).  4096 slots of
+// 16 words = 512 KB per context; ~3 slots per distributed level.
+#define AMGP_MAX_SLOTS 4096
 // per-slot synchronisation words of the p2p transport (u64, monotonic):
 //   [0, nranks)         ready[src]    -- epoch of the last halo src delivered here
 //   [nranks, 2 nranks)  consumed[dst] -- epoch whose halo dst has finished reading
 //   [2 nranks]          epoch         -- exchanges completed on this rank
 //   [2 nranks + 1]      ticket        -- pack-kernel CTAs done (last one signals)
 //   [2 nranks + 2]      ticket        -- boundary launch CTAs done (last one completes)
-//   fused launch counters, in their own 128-byte line (they take an atomic
-//   from every pack / boundary warp; the words above are polled across GPUs):
-//   [ctr + 0]           ticket        -- counted CTAs done (last one completes)
-//   [ctr + 1]           counter       -- pack chunks claimed
-//   [ctr + 2]           counter       -- pack chunks stored
-#define AMGP_SYNC_CTR(nr) ((2 * (nr) + 3 + 15) / 16 * 16)
-#define AMGP_SYNC_STRIDE(nr) (AMGP_SYNC_CTR(nr) + 16)
+#define AMGP_SYNC_STRIDE(nr) ((2 * (nr) + 3 + 15) / 16 * 16)
 
 // Halo plan of a row-distributed matrix (dist.cu).  Columns [0, nown) are
 // the rank's own entries of the operand vector; columns >= nown index the
@@ -118,7 +111,6 @@ struct HaloPlan {
     std::vector<std::pair<int64_t, int64_t>> interior_runs, boundary_runs;
     // p2p transport: sync slot, per-peer remote destinations of my data
     int slot = -1;
-    bool fused = false;              // one ROWS_FUSED launch per SpMV, halo double-buffered
     bool sym = false;                // every send peer is also a receive peer
     double **d_dest = nullptr;       // device [2 npeers] remote base for my segment (parity 0, then 1)
     int64_t *d_seg = nullptr;        // device [npeers + 1] send offsets
@@ -164,32 +156,15 @@ struct SellView {
     int nruns;
     int64_t run_s0[SELL_RUNS], run_end[SELL_RUNS];
     // p2p transport: before gathering xh, wait until every rank in recvp has
-    // delivered this exchange (sync words of the matrix slot, amgp_ctx);
-    // fused launches: indices < nfirst are interior slices, and the last CTA
-    // signals consumed_remote (halo_complete)
+    // delivered this exchange (sync words of the matrix slot, amgp_ctx); the
+    // halo is double-buffered by exchange parity: exchange e lives at
+    // xh + (e & 1) * xh_stride
     unsigned long long *sync_slot;
     const int *recvp;
     int nrecvp, nranks;
-    int fused;
     int complete;  // ROWS_GEN boundary launch of the p2p transport: last CTA completes
-    int64_t nfirst;
     unsigned long long *const *consumed_remote;
-    // fused launch (ROWS_FUSED): launch indices < npack are pack CTAs; the
-    // halo is double-buffered -- exchange e lives at xh + (e & 1) * xh_stride
-    // and my segment for peer q at dest[(e & 1) * npeers + q]
-    int npack;
-    int npeers;
-    int sym;      // every rank I send to also sends to me: the consumed wait is implied
-    int ctr;      // AMGP_SYNC_CTR(nranks)
-    int64_t ncounted;  // pack CTAs + CTAs that wait for the halo
-    int64_t nsend;
     int64_t xh_stride;
-    const int64_t *__restrict__ send_idx;
-    const int64_t *__restrict__ seg;
-    double *const *__restrict__ dest;
-    const int *sendp;
-    int nsendp;
-    unsigned long long *const *ready_remote;
 };
 
 inline SellView view_of(const amgp_mat *A) {
@@ -259,10 +234,9 @@ __device__ __forceinline__ const double *halo_wait(const SellView &A) {
     return A.xh + (int64_t)(e & 1ull) * A.xh_stride;
 }
 
-// End of a fused p2p launch, called by the nctas CTAs that waited for the
-// halo: the last of them advances the epoch and tells every sender its halo
-// has been read (all reads precede the ticket; interior CTAs neither wait
-// nor count, so the ticket costs one atomic per boundary CTA).
+// End of a boundary launch of the p2p transport, called by its nctas CTAs:
+// the last of them advances the epoch and tells every sender its halo has
+// been read (all reads precede the ticket).
 __device__ __forceinline__ void halo_complete(const SellView &A, unsigned nctas) {
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -279,132 +253,11 @@ __device__ __forceinline__ void halo_complete(const SellView &A, unsigned nctas)
     }
 }
 
-// ---- fused launch (ROWS_FUSED): pack, wait and completion inside the SpMV grid
-//
-// Exchange e of a matrix slot (e = epoch word, exchanges completed here) uses
-// halo buffer parity e & 1.  Pack: the operand entries each neighbour needs
-// are stored straight into its parity-(e & 1) buffer, after it has finished
-// reading exchange e - 2 from that buffer (consumed >= e - 1); the CTA that
-// stores the last chunk publishes ready = e + 1 to every receiver.  Pack work
-// is a pool of chunks claimed with an atomic counter, by the pack CTAs (the
-// lowest launch indices, so in practice the pack is done first) AND by every
-// boundary CTA before it waits: a CTA that spins for a halo has already
-// drained its own rank's pack, so the wait never depends on CTAs that might
-// not be resident.  Boundary CTAs then wait ready >= e + 1 from every sender
-// and gather through the parity buffer.  Pack and boundary CTAs are counted;
-// the last one advances the epoch, resets the counters and publishes
-// consumed = e + 1 to every sender.  Interior CTAs neither wait nor count.
-// Launches of one slot run in the same order on every rank, a sender's pack
-// for e waits only on exchange e - 1, so no wait can close a cycle.
-#define FUSED_PACK_U 8  // send entries per lane per chunk
-#ifndef FUSED_DIAG
-#define FUSED_DIAG 0  // timing experiments only: 1 no halo wait, 2 no pack + no wait, 3 no completion fences,
-                      // 4 pack stores to a local buffer
-#endif
-
-// epoch of the slot (read per warp: it changes only after every counted CTA
-// has finished, see fused_complete)
-__device__ __forceinline__ unsigned long long fused_epoch(const SellView &A) {
-    unsigned long long e = 0;
-    // (written by this GPU's previous launch of the slot: no cross-GPU ordering needed)
-    if ((threadIdx.x & 31) == 0) e = ld_relaxed_gpu(A.sync_slot + 2 * A.nranks);
-    return __shfl_sync(0xffffffffu, e, 0);
-}
-
-// Pack chunks (32 * FUSED_PACK_U send entries, every load of a chunk in
-// flight at once: the pack runs next to a bandwidth-saturating interior, so
-// each dependent round costs microseconds) are claimed per WARP, so the pack
-// needs no shared memory and no CTA barrier.
-#define FUSED_CHUNK (32 * FUSED_PACK_U)
-__device__ __forceinline__ void fused_pack(const SellView &A, unsigned long long e,
-                                           const double *__restrict__ x) {
-    if (A.nsend == 0 || FUSED_DIAG == 2) return;
-    unsigned long long *sync = A.sync_slot;
-    const int lane = threadIdx.x & 31;
-    const long long nchunks = (long long)((A.nsend + FUSED_CHUNK - 1) / FUSED_CHUNK);
-    const int par = (int)(e & 1ull);
-    long long mine = 0;
-    for (;;) {
-        long long c = 0;
-        if (lane == 0) {
-            c = (long long)atomicAdd(sync + A.ctr + 1, 1ull);
-            // receivers done with exchange e - 2 (same parity).  Implied when
-            // every receiver also sends to me: my launch e - 1 waited for its
-            // exchange e - 1, packed after its launch e - 2 had completed.
-            if (c < nchunks && mine == 0 && !A.sym && e >= 2) {
-                for (int i = 0; i < A.nsendp; i++) {
-                    const unsigned long long *w = sync + A.nranks + A.sendp[i];
-                    while (ld_relaxed_sys(w) + 1 < e) __nanosleep(64);
-                    (void)ld_acquire_sys(w);
-                }
-            }
-        }
-        c = __shfl_sync(0xffffffffu, c, 0);
-        if (c >= nchunks) break;
-        mine++;
-        const int64_t i0 = c * FUSED_CHUNK + lane;
-        int64_t idx[FUSED_PACK_U];
-        double v[FUSED_PACK_U];
-#pragma unroll
-        for (int u = 0; u < FUSED_PACK_U; u++) {
-            const int64_t i = i0 + 32 * u;
-            idx[u] = i < A.nsend ? A.send_idx[i] : -1;
-        }
-#pragma unroll
-        for (int u = 0; u < FUSED_PACK_U; u++) v[u] = idx[u] >= 0 ? x[idx[u]] : 0.0;
-#pragma unroll
-        for (int u = 0; u < FUSED_PACK_U; u++) {
-            const int64_t i = i0 + 32 * u;
-            if (i < A.nsend) {
-                int q = 0;
-                while (q + 1 < A.npeers && i >= A.seg[q + 1]) q++;
-                if (FUSED_DIAG == 4) ((double *)A.xh)[i % max(A.xh_stride, (int64_t)1)] = v[u];
-                else A.dest[par * A.npeers + q][i - A.seg[q]] = v[u];
-            }
-        }
-    }
-    if (mine == 0) return;
-    __syncwarp();
-    if (lane == 0) {
-        __threadfence_system();
-        if ((long long)atomicAdd(sync + A.ctr + 2, (unsigned long long)mine) + mine == nchunks)
-            for (int i = 0; i < A.nsendp; i++) st_release_sys(A.ready_remote[i], e + 1);
-    }
-}
-
-__device__ __forceinline__ void fused_wait(const SellView &A, unsigned long long e) {
-    if (A.nrecvp == 0 || FUSED_DIAG == 1 || FUSED_DIAG == 2) return;
-    if (threadIdx.x == 0)
-        for (int i = 0; i < A.nrecvp; i++) {
-            const unsigned long long *w = A.sync_slot + A.recvp[i];
-            while (ld_relaxed_sys(w) < e + 1) __nanosleep(20);
-            (void)ld_acquire_sys(w);
-        }
-    __syncthreads();
-}
-
-__device__ __forceinline__ void fused_complete(const SellView &A, unsigned long long e, unsigned ncounted) {
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        unsigned long long *sync = A.sync_slot;
-        if (FUSED_DIAG != 3) __threadfence();
-        if (atomicAdd(sync + A.ctr, 1ull) == ncounted - 1) {
-            sync[A.ctr] = 0;
-            sync[A.ctr + 1] = 0;
-            sync[A.ctr + 2] = 0;
-            sync[2 * A.nranks] = e + 1;
-            __threadfence_system();
-            for (int i = 0; i < A.nrecvp; i++) st_release_sys(A.consumed_remote[i], e + 1);
-        }
-    }
-}
-
 // Exchange the halo of operand x (own part) for a distributed matrix; after
 // it, kernels may gather x through view.xh (dist.cu).
 int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x);
 int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A);
 int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A);  // after the boundary rows
-int halo_exchange_wait_done(amgp_ctx *ctx, const amgp_mat *A);  // exchange-only: wait, then complete
 void mat_free_halo(amgp_mat *A);
 void ctx_free_comm(amgp_ctx *ctx);  // communicator resources (amgp_ctx_destroy)
 int refresh_slice_maxcol(amgp_mat *A);  // recompute A->slice_maxcol from the device columns
@@ -471,6 +324,15 @@ __device__ __forceinline__ double ld_gather_f64(const double *p, uint64_t pol) {
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
+// Halo entries are written by a peer GPU while the kernel runs (p2p
+// transport): never through the non-coherent path, never hoisted above the
+// in-kernel halo wait (volatile, ordered after its acquire + barrier), and
+// cached at L2 only (the point of coherence for the peer's NVLink stores).
+__device__ __forceinline__ double ld_halo_f64(const double *p) {
+    double v;
+    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
 
 // Row sum of slice row `lane` of slice `s`: sum_j val*x[col] from 0.0 in slot
 // order (== CSR stored order).  Slots are loaded U at a time (predicated) so
@@ -500,12 +362,10 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
 #pragma unroll
         for (int u = 0; u < U; u++) {
             if (HALO) {
-                // branch-free operand select (own vector or halo buffer), so
-                // the U gathers stay one predicated batch
+                // own entries through the read-only path, halo entries
+                // coherently (ld_halo_f64)
                 const int64_t c = cc[u];
-                const bool own = c < A.nown;
-                const double *p = (own ? x : xh) + (own ? c : c - A.nown);
-                xx[u] = cc[u] < 0 ? 0.0 : ld_gather_f64(p, pl);
+                xx[u] = c < 0 ? 0.0 : (c < A.nown ? ld_gather_f64(x + c, pl) : ld_halo_f64(xh + (c - A.nown)));
             } else
                 xx[u] = cc[u] < 0 ? 0.0 : ld_gather_f64(x + cc[u], pl);
         }

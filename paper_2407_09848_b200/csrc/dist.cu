@@ -36,11 +36,6 @@
 //   boundary rows       wait ready[src] >= epoch + 1 (acquire.sys) first
 //   completion          epoch += 1 and consumed[me] = epoch on every sender:
 //                       the boundary launch's last CTA, else k_halo_signal
-// AMGP_P2P_FUSED=1, for matrices whose slice sets are a few runs: the fused
-// launch (amgp_common.cuh "fused launch", rows.cuh ROWS_FUSED) -- pack,
-// interior, boundary and completion in ONE grid, halo double-buffered by
-// epoch parity.  Correct (GPU tests) but measured slower than the default
-// pack kernel + boundary launch.
 // Exchange order is the same on every rank (SPMD), so no wait can close a
 // cycle; everything is an ordinary kernel and is captured into graphs.
 struct NcclApi {
@@ -192,13 +187,8 @@ extern "C" int amgp_ctx_init_comm(amgp_ctx *ctx, int nranks, int rank, const cha
     // halo transport: direct NVLink (default when every pair of GPUs can
     // map each other, <= 64 ranks) or NCCL (AMGP_HALO=nccl, or fallback)
     const char *mode = getenv("AMGP_HALO");
-    if (mode && strcmp(mode, "skip") == 0) ctx->halo_p2p = -1;  // diagnostic: no transfer (stale halo)
     const bool want_p2p = !mode || strcmp(mode, "p2p") == 0;
-    if (want_p2p && nranks > 1 && nranks <= 64) {
-        AMGP_TRY(p2p_init(ctx));
-        const char *fz = getenv("AMGP_P2P_FUSED");
-        ctx->p2p_fused = fz ? atoi(fz) : 0;
-    }
+    if (want_p2p && nranks > 1 && nranks <= 64) AMGP_TRY(p2p_init(ctx));
     return AMGP_OK;
 }
 
@@ -233,6 +223,11 @@ extern "C" int amgp_ctx_comm_info(amgp_ctx *ctx, int *nranks, int *rank) {
 }
 
 // ---------------------------------------------------------------- halo plans
+// Freeing a plan needs no cross-rank barrier under SPMD use: every peer's
+// pack into my halo buffer for an exchange completes before my boundary
+// launch of that exchange (which waits for it), so after my stream is idle no
+// peer writes my halo buffers; the peers' last consumed/ready signals land in
+// the context's sync words, which live as long as the context.
 static void halo_free(HaloPlan *h) {
     if (!h) return;
     for (void *p : h->opened) cudaIpcCloseMemHandle(p);
@@ -257,29 +252,27 @@ void mat_free_halo(amgp_mat *A) {
 
 // Map where this rank's data lands in each receiver's halo buffer.
 static int p2p_attach(amgp_ctx *ctx, HaloPlan *h) {
-    if (ctx->next_slot >= AMGP_MAX_SLOTS) return amgp_fail(AMGP_EINVAL, "too many distributed matrices");
+    if (ctx->next_slot >= AMGP_MAX_SLOTS)
+        return amgp_fail(AMGP_EINVAL, "too many distributed matrices on this context: all " +
+                                          std::to_string(AMGP_MAX_SLOTS) +
+                                          " p2p synchronisation slots are used (slots are not reused)");
     h->slot = ctx->next_slot++;
     struct Info {
         cudaIpcMemHandle_t handle;
         int64_t recv_off[64];
         int64_t recv_cnt[64];
         int64_t nhalo;
-        int fused;
     };
     Info mine;
     memset(&mine, 0, sizeof(mine));
     AMGP_CUDA(cudaIpcGetMemHandle(&mine.handle, h->halo));
     mine.nhalo = h->nhalo;
-    mine.fused = h->fused;
     for (size_t q = 0; q < h->peers.size(); q++) {
         mine.recv_off[h->peers[q]] = h->recv_off[q];
         mine.recv_cnt[h->peers[q]] = h->recv_cnt[q];
     }
     std::vector<char> all;
     AMGP_TRY(allgather_host(ctx, &mine, sizeof(Info), all));
-    // the fused launch changes the protocol (double buffer), so every rank
-    // must agree on it for this slot
-    for (int r = 0; r < ctx->nranks; r++) h->fused &= ((const Info *)all.data())[r].fused != 0;
     const size_t np = h->peers.size();
     std::vector<double *> dest(2 * np, nullptr);
     std::vector<int64_t> seg(np + 1, 0);
@@ -395,9 +388,7 @@ extern "C" int amgp_mat_set_halo(amgp_mat *A, int64_t nown, int npeers, const in
     up((void **)&h->interior, in.data(), in.size() * sizeof(int32_t));
     up((void **)&h->boundary, bd.data(), bd.size() * sizeof(int32_t));
     if (e == cudaSuccess) e = cudaMalloc(&h->sendbuf, std::max<int64_t>(so, 1) * sizeof(double));
-    // p2p: two halo buffers (exchange parity) for the fused launch
-    h->fused = ctx->halo_p2p > 0 && ctx->p2p_fused &&
-               h->interior_runs.size() + h->boundary_runs.size() <= SELL_RUNS;
+    // p2p: two halo buffers (exchange parity, see k_pack_p2p)
     if (e == cudaSuccess)
         e = cudaMalloc(&h->halo, std::max<int64_t>(ro, 1) * (ctx->halo_p2p > 0 ? 2 : 1) * sizeof(double));
     if (e != cudaSuccess) {
@@ -486,30 +477,6 @@ __global__ void k_halo_signal(unsigned long long *sync, int nranks, int nrecvp,
     for (int i = 0; i < nrecvp; i++) st_release_sys(consumed_remote[i], e);
 }
 
-// exchange-only diagnostic: wait for this exchange's halo, then complete it
-__global__ void k_halo_wait_signal(unsigned long long *sync, int nranks, const int *__restrict__ recvp,
-                                   int nrecvp, unsigned long long *const *__restrict__ consumed_remote) {
-    if (threadIdx.x != 0) return;
-    const unsigned long long e = sync[2 * nranks] + 1;
-    for (int i = 0; i < nrecvp; i++) {
-        while (ld_relaxed_sys(sync + recvp[i]) < e) __nanosleep(20);
-        (void)ld_acquire_sys(sync + recvp[i]);
-    }
-    sync[2 * nranks] = e;
-    __threadfence_system();
-    for (int i = 0; i < nrecvp; i++) st_release_sys(consumed_remote[i], e);
-}
-
-int halo_exchange_wait_done(amgp_ctx *ctx, const amgp_mat *A) {
-    if (ctx->halo_p2p <= 0) return AMGP_OK;
-    const HaloPlan &h = *A->halo;
-    if (h.peers.empty()) return AMGP_OK;
-    k_halo_wait_signal<<<1, 32, 0, ctx->stream>>>(h.sync_slot, ctx->nranks, h.d_recvp, h.nrecvp,
-                                                  h.d_consumed_remote);
-    AMGP_CHECK_LAUNCH(ctx);
-    return AMGP_OK;
-}
-
 static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
     if (h.nsend == 0) return AMGP_OK;
     cudaStream_t st = ctx->comm_stream;
@@ -543,7 +510,7 @@ static int p2p_end(amgp_ctx *ctx, const HaloPlan &h) {
 }
 
 int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A) {
-    if (ctx->halo_p2p <= 0) return AMGP_OK;
+    if (!ctx->halo_p2p) return AMGP_OK;
     const HaloPlan &h = *A->halo;
     if (h.peers.empty()) return AMGP_OK;
     k_halo_signal<<<1, 32, 0, ctx->stream>>>(h.sync_slot, ctx->nranks, h.nrecvp, h.d_consumed_remote);
@@ -553,7 +520,6 @@ int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A) {
 
 int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
     const HaloPlan &h = *A->halo;
-    if (ctx->halo_p2p < 0) return AMGP_OK;
     if (ctx->halo_p2p) return p2p_begin(ctx, h, x);
     NcclApi *api = nccl();
     if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator for the halo exchange");
@@ -580,7 +546,6 @@ int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
 }
 
 int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A) {
-    if (ctx->halo_p2p < 0) return AMGP_OK;
     if (ctx->halo_p2p) return p2p_end(ctx, *A->halo);
     AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
     return AMGP_OK;

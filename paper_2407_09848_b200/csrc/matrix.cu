@@ -127,6 +127,7 @@ extern "C" int amgp_mat_destroy(amgp_mat *A) {
     if (A->ctx) {
         cudaSetDevice(A->ctx->device);
         cudaStreamSynchronize(A->ctx->stream);
+        if (A->ctx->comm_stream) cudaStreamSynchronize(A->ctx->comm_stream);  // halo pack kernels
     }
     mat_free_halo(A);
     cudaFree(A->slice_ptr);
@@ -402,67 +403,6 @@ int residual_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *r, const do
 }
 int prolong_add_enqueue(amgp_ctx *ctx, const amgp_mat *P, const double *xc, double *x) {
     return launch_rows(ctx, P, xc, SpmvEpi<2>{nullptr, x});
-}
-
-// Diagnostics: reps back-to-back SpMVs (halo exchanges included for a
-// distributed matrix), captured once into a CUDA graph when use_graph & 1,
-// timed with CUDA events on the context stream.  *ms = milliseconds per
-// SpMV.  use_graph & 2: only the halo exchanges (transport latency).
-static int exchange_only(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
-    if (!A->halo) return AMGP_OK;
-    if (A->halo->fused) {  // fused protocol: a launch of pack CTAs + one waiting CTA, no rows
-        SellView v = view_of(A);
-        fused_view(ctx, A, v);
-        v.nruns = 0;
-        v.nlist = 0;
-        v.nfirst = 0;
-        return launch_view(ctx, A, v, x, SpmvEpi<0>{nullptr, nullptr});
-    }
-    AMGP_TRY(halo_exchange_begin(ctx, A, x));
-    AMGP_TRY(halo_exchange_end(ctx, A));
-    return ctx->halo_p2p > 0 ? halo_exchange_wait_done(ctx, A) : halo_exchange_done(ctx, A);
-}
-
-extern "C" int amgp_spmv_timed(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y,
-                               int reps, int flags, double *ms) {
-    if (!ctx || !A || reps < 1 || !ms) return amgp_fail(AMGP_EINVAL, "amgp_spmv_timed: bad argument");
-    const bool use_graph = flags & 1, xonly = flags & 2;
-    auto one = [&]() { return xonly ? exchange_only(ctx, A, x) : spmv_enqueue(ctx, A, x, y); };
-    AMGP_CUDA(cudaSetDevice(ctx->device));
-    cudaEvent_t e0, e1;
-    AMGP_CUDA(cudaEventCreate(&e0));
-    AMGP_CUDA(cudaEventCreate(&e1));
-    cudaGraphExec_t exec = nullptr;
-    if (use_graph) {
-        cudaGraph_t g = nullptr;
-        AMGP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
-        int st = AMGP_OK;
-        for (int i = 0; i < reps && st == AMGP_OK; i++) st = one();
-        cudaError_t e = cudaStreamEndCapture(ctx->stream, &g);
-        if (st != AMGP_OK) return st;
-        if (e != cudaSuccess) return amgp_cuda_fail(e, "capture", __FILE__, __LINE__);
-        AMGP_CUDA(cudaGraphInstantiate(&exec, g, 0));
-        cudaGraphDestroy(g);
-        AMGP_CUDA(cudaGraphLaunch(exec, ctx->stream));  // warm-up
-    } else {
-        AMGP_TRY(one());
-    }
-    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
-    AMGP_CUDA(cudaEventRecord(e0, ctx->stream));
-    if (use_graph) {
-        AMGP_CUDA(cudaGraphLaunch(exec, ctx->stream));
-    } else {
-        for (int i = 0; i < reps; i++) AMGP_TRY(one());
-    }
-    AMGP_CUDA(cudaEventRecord(e1, ctx->stream));
-    AMGP_CUDA(cudaEventSynchronize(e1));
-    float t = 0.f;
-    AMGP_CUDA(cudaEventElapsedTime(&t, e0, e1));
-    *ms = t / reps;
-    if (exec) cudaGraphExecDestroy(exec);
-    cudaEventDestroy(e0);
-    cudaEventDestroy(e1);
-    return AMGP_OK;
 }
 
 extern "C" int amgp_spmv(amgp_ctx *ctx, const amgp_mat *A, const double *x, double *y) {

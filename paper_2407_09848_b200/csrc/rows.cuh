@@ -37,12 +37,8 @@
 // Launch modes.  ROWS_PLAIN: slices of the run table, every column local
 // (single-GPU matrices, interior slices of distributed ones).  ROWS_GEN: a
 // slice list and/or halo columns (boundary slices) -- kept out of the common
-// kernel so its gather stays one load per slot.  ROWS_FUSED (p2p transport,
-// amgp_common.cuh "fused launch"): launch indices < npack pack the operand
-// into the neighbours' halo buffers; the rest are slices of the run table,
-// interior first (plain gather, no wait), then boundary (pack help, in-kernel
-// halo wait, gather through the parity buffer).  CTA-uniform branches.
-enum { ROWS_PLAIN = 0, ROWS_GEN = 1, ROWS_FUSED = 2 };
+// kernel so its gather stays one load per slot.
+enum { ROWS_PLAIN = 0, ROWS_GEN = 1 };
 
 // Rows of launch CTA `cta` (ROWS_SLICES slices): y = A x (halo-aware gather
 // when HALO), then the epilogue.
@@ -65,26 +61,10 @@ __global__ void __launch_bounds__(ROWS_BLOCK, 8)  // 32 registers: 8 CTAs per SM
 k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     if (MODE == ROWS_PLAIN) {
         thread_rows_body<Epi, MODE, false>(A, blockIdx.x, xg, nullptr, epi);
-    } else if (MODE == ROWS_GEN) {
+    } else {
         const double *xh = halo_wait(A);
         thread_rows_body<Epi, MODE, true>(A, blockIdx.x, xg, xh, epi);
         if (A.complete) halo_complete(A, gridDim.x);
-    } else {
-        // separate paths, so the interior rows keep the plain kernel's registers
-        const int64_t cta = (int64_t)blockIdx.x - A.npack;
-        if (cta < 0) {  // pack CTA
-            const unsigned long long e = fused_epoch(A);
-            fused_pack(A, e, xg);
-            fused_complete(A, e, (unsigned)A.ncounted);
-        } else if ((cta + 1) * ROWS_SLICES <= A.nfirst) {  // interior slices only
-            thread_rows_body<Epi, MODE, false>(A, cta, xg, nullptr, epi);
-        } else {  // boundary: help the pack, wait for the halo, gather through it
-            const unsigned long long e = fused_epoch(A);
-            fused_pack(A, e, xg);
-            fused_wait(A, e);
-            thread_rows_body<Epi, MODE, true>(A, cta, xg, A.xh + (int64_t)(e & 1ull) * A.xh_stride, epi);
-            fused_complete(A, e, (unsigned)A.ncounted);
-        }
     }
 }
 
@@ -96,30 +76,10 @@ template <class Epi, int MODE, int NW, int U>
 __global__ void __launch_bounds__(NW * 32)
 k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     __shared__ double prod[SPLIT_CHUNK * 32];
-    int64_t cta = blockIdx.x;
-    unsigned long long e = 0;
-    if (MODE == ROWS_FUSED) {
-        if (cta < A.npack) {
-            e = fused_epoch(A);
-            fused_pack(A, e, xg);
-            fused_complete(A, e, (unsigned)A.ncounted);
-            return;
-        }
-        cta -= A.npack;
-    }
-    const bool halo = MODE == ROWS_GEN || (MODE == ROWS_FUSED && cta >= A.nfirst);
+    const int64_t cta = blockIdx.x;
+    const bool halo = MODE == ROWS_GEN;
     const double *xh = A.xh;
     if (MODE == ROWS_GEN) xh = halo_wait(A);
-    if (MODE == ROWS_FUSED && halo) {
-        e = fused_epoch(A);
-        fused_pack(A, e, xg);
-        fused_wait(A, e);
-        xh += (int64_t)(e & 1ull) * A.xh_stride;
-        if (cta >= A.nlist) {  // exchange-only launch: wait and complete, no rows
-            fused_complete(A, e, (unsigned)A.ncounted);
-            return;
-        }
-    }
     const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[cta] : run_slice(A, cta);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = A.slice_ptr[s];
@@ -144,11 +104,13 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                 const int jj = j + u * NW;
                 if (jj < jn) {
                     double p = 0.0;
-                    // branch-free operand select (own vector or halo buffer)
+                    // own entries through the read-only path, halo entries coherently
                     const int64_t c = cc[u];
-                    const bool hc = MODE != ROWS_PLAIN && halo && c >= A.nown;
-                    const double *src = (hc ? xh : xg) + (hc ? c - A.nown : c);
-                    if (cc[u] >= 0) p = __dmul_rn(vv[u], ld_gather_f64(src, pl));
+                    if (c >= 0) {
+                        const double xv = halo && c >= A.nown ? ld_halo_f64(xh + (c - A.nown))
+                                                              : ld_gather_f64(xg + c, pl);
+                        p = __dmul_rn(vv[u], xv);
+                    }
                     prod[jj * 32 + lane] = p;
                 }
             }
@@ -164,7 +126,6 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
         const int64_t row = s * 32 + lane;
         if (row < A.nrows) epi(row, sum);
     }
-    if (MODE == ROWS_FUSED && halo) fused_complete(A, e, (unsigned)A.ncounted);
     if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }
 
@@ -176,12 +137,6 @@ inline bool use_split(const amgp_mat *A, int64_t nslices_launched) {
     return A->max_width >= 24 && nslices_launched < 148 * 64;
 }
 
-// pack CTAs of a fused launch with block size bs: one per chunk, <= 1 per SM
-inline int fused_npack(const SellView &v, int bs) {
-    const int64_t csize = (int64_t)(bs / 32) * FUSED_CHUNK;
-    return (int)std::min<int64_t>((v.nsend + csize - 1) / csize, 148);
-}
-
 template <class Epi, int MODE>
 void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const double *xg,
                  const Epi &epi) {
@@ -189,14 +144,7 @@ void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const dou
     const bool split = Epi::kSpmv && use_split(A, v.nlist);
     const int nw = v.nlist < 2 * 148 ? 24 : SPLIT_WARPS;
     const int bs = split ? nw * 32 : ROWS_BLOCK;
-    unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);
-    if (MODE == ROWS_FUSED) {  // pack CTAs first; at least one CTA waits and completes
-        v.npack = fused_npack(v, bs);
-        const int64_t first_bnd = split ? v.nfirst : v.nfirst / ROWS_SLICES;  // first waiting CTA
-        const int64_t nrow_ctas = std::max<int64_t>(grid, first_bnd + 1);
-        v.ncounted = v.npack + (nrow_ctas - first_bnd);
-        grid = (unsigned)(v.npack + nrow_ctas);
-    }
+    const unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);
     if (split) {
         if (nw == 24)
             k_split_rows<Epi, MODE, 24, 8><<<grid, 24 * 32, 0, ctx->stream>>>(v, xg, epi);
@@ -210,57 +158,18 @@ void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const dou
 template <class Epi>
 int launch_view(amgp_ctx *ctx, const amgp_mat *A, const SellView &v, const double *xg,
                 const Epi &epi) {
-    if (v.nlist == 0 && !v.fused) return AMGP_OK;
-    if (v.fused) launch_mode<Epi, ROWS_FUSED>(ctx, A, v, xg, epi);
-    else if (v.slist || v.xh) launch_mode<Epi, ROWS_GEN>(ctx, A, v, xg, epi);
+    if (v.nlist == 0) return AMGP_OK;
+    if (v.slist || v.xh) launch_mode<Epi, ROWS_GEN>(ctx, A, v, xg, epi);
     else launch_mode<Epi, ROWS_PLAIN>(ctx, A, v, xg, epi);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
-}
-
-// Fill the fused-launch fields of a view of distributed matrix A (runs:
-// interior then boundary; HaloPlan::fused).
-inline void fused_view(amgp_ctx *ctx, const amgp_mat *A, SellView &v) {
-    const HaloPlan &h = *A->halo;
-    v.sync_slot = h.sync_slot;
-    v.recvp = h.d_recvp;
-    v.nrecvp = h.nrecvp;
-    v.nranks = ctx->nranks;
-    v.consumed_remote = h.d_consumed_remote;
-    v.slist = nullptr;
-    v.nruns = 0;
-    int64_t end = 0;
-    for (const auto *set : {&h.interior_runs, &h.boundary_runs})
-        for (const auto &r : *set) {
-            v.run_s0[v.nruns] = r.first;
-            end += r.second;
-            v.run_end[v.nruns++] = end;
-        }
-    v.nlist = end;
-    v.fused = 1;
-    v.nfirst = h.n_interior;
-    v.nown = h.nown;
-    v.xh = h.halo;
-    v.xh_stride = h.nhalo;
-    v.npeers = (int)h.peers.size();
-    v.nsend = h.nsend;
-    v.send_idx = h.send_idx;
-    v.seg = h.d_seg;
-    v.dest = h.d_dest;
-    v.sendp = h.d_sendp;
-    v.nsendp = h.nsendp;
-    v.ready_remote = h.d_ready_remote;
-    v.sym = h.sym;
-    v.ctr = AMGP_SYNC_CTR(ctx->nranks);
 }
 
 // y-rows of A with epilogue epi, gathering operand xg.  For a distributed
 // matrix the halo of xg travels while the interior slices (no halo column)
 // compute: interior launch, exchange (NCCL on the comm stream, or the p2p
 // pack kernel on the high-priority stream), boundary launch (p2p: in-kernel
-// waits; it completes the exchange).  AMGP_P2P_FUSED=1 (HaloPlan::fused):
-// ONE ROWS_FUSED launch (pack CTAs, interior slices, boundary slices that
-// wait for the halo in-kernel) when the slice sets are a few runs.
+// waits; it completes the exchange).
 template <class Epi>
 int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &epi) {
     if (!Epi::kSpmv || !A->halo) {
@@ -271,10 +180,6 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     const bool p2p = ctx->halo_p2p > 0;
     if (A->nslices == 0 && !p2p) return AMGP_OK;
     SellView v = view_of(A);
-    if (h.fused) {
-        fused_view(ctx, A, v);
-        return launch_view(ctx, A, v, xg, epi);
-    }
     AMGP_TRY(halo_exchange_begin(ctx, A, xg));
     if (p2p) {
         v.sync_slot = h.sync_slot;

@@ -11,47 +11,10 @@
 // single-CTA kernel (K6) with the iterate in shared memory when it fits, else
 // one launch per sweep; or the dense Cholesky solve.
 // The whole V-cycle is captured once into a CUDA graph and replayed.
-#include <cooperative_groups.h>
-
 #include <algorithm>
 #include <vector>
 
 #include "epilogues.cuh"
-
-namespace cg = cooperative_groups;
-
-// ---------------------------------------------------------------- V-cycle tail
-// The smallest levels of a hierarchy are latency bound: ~20 us per launch for
-// a few thousand rows.  K8 runs the whole bottom of the V-cycle (pre-smooth,
-// residual, restriction on every tail level, the coarse solve, prolongation
-// and post-smoothing back up) as ONE cooperative kernel: one CTA per SM, every
-// step a grid-wide phase separated by grid.sync().  Within a phase each CTA
-// takes whole 32-row slices, forms all (row, slot) products in parallel into
-// shared memory and sums each row in slot order -- the per-row arithmetic of
-// the regular kernels, so the results are bitwise unchanged.
-#define TAIL_MAX_LEV 8
-#define TAIL_MAX_K 32
-#define TAIL_THREADS 512
-#define TAIL_CHUNK 192
-#define TAIL_MAX_STORED (4LL << 20)
-#define TAIL_MAX_ROWS 65536
-
-struct TailLev {
-    SellView A, P, R;  // P: this level <- next; R: next <- this
-    const double *m;
-    const double *r;   // rhs (levels >= 1 of the tail; level 0 comes as a kernel argument)
-    double *z, *xpre, *res, *work;
-    int64_t n;
-    int wA, wP, wR;  // widest slice of A, P, R (picks the phase schedule)
-    int family, degree;
-    double rho;
-    double coef[3 * TAIL_MAX_K];
-};
-
-struct TailDesc {
-    int nlev, coarse_sweeps;
-    TailLev lev[TAIL_MAX_LEV];
-};
 
 struct amgp_hier {
     amgp_ctx *ctx = nullptr;
@@ -71,25 +34,10 @@ struct amgp_hier {
     const double *g_r = nullptr;
     double *g_z = nullptr;
     int64_t g_nodes = 0;
-    // cooperative tail (K8)
-    // Off by default: measured on B200 (128^3 SA, levels 3-5 in the tail)
-    // 12.4 ms vs 11.6 ms per solve -- the grid barriers plus the sequential
-    // 300-500-term row sums of the coarse SA levels cost more than the
-    // launches they replace (profiles/r01_summary.md).
-    bool use_tail = false;
-    bool tail_dirty = true;
-    int tail_start = -1;  // first level run by the tail kernel (-1: none)
-    TailDesc *d_tail = nullptr;
-    size_t tail_smem = 0;
-    int tail_grid = 0;
     std::mutex mu;
 };
 
 #define COARSE_SMEM_BYTES (227 * 1024)
-#define TAIL_COARSE_SMEM (200 * 1024)  // K8's coarse phase (products staged)
-static inline size_t tail_coarse_smem(const amgp_mat *A) {
-    return 16 * (size_t)A->nrows + 20 * (size_t)A->stored + 64;
-}
 
 // K6 for coarsest levels too large for k_coarse_l1_reg (below): all
 // l1-Jacobi sweeps in one CTA with the level's SELL values and columns staged
@@ -257,304 +205,7 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
     return smoother_enqueue(ctx, A, h->m[l], h->coarse_plan, r, nullptr, z, h->work[l]);
 }
 
-// ---------------------------------------------------------------- K8 device side
-// One grid-wide phase: y = A xg row by row, then epi(row, y).  Short rows
-// (the matrix's widest slice <= TAIL_SHORT slots): every thread of the grid
-// owns rows (a warp = one slice) and sums its slots in order.  Long rows: a
-// CTA owns a slice, its warps form the slot products (8 independent loads in
-// flight per thread) into shared memory, warp 0 sums them in slot order.
-// Operands written by earlier phases are read with ld.global.cg (L2), never
-// through the non-coherent path.
-#define TAIL_SHORT 16
-template <class Epi>
-__device__ void tail_phase(const SellView &A, int wmax, const double *xg, const Epi &epi,
-                           double *prod) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    if (!Epi::kSpmv || wmax <= TAIL_SHORT) {
-        const int64_t nthr = (int64_t)gridDim.x * blockDim.x;
-        for (int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; row < A.nslices * 32;
-             row += nthr) {
-            double y = 0.0;
-            if (Epi::kSpmv) {
-                const int64_t s = row >> 5, base = __ldg(A.slice_ptr + s);
-                const int w = (int)((__ldg(A.slice_ptr + s + 1) - base) >> 5);
-                const int32_t *cp = A.col + base + (row & 31);
-                const double *vp = A.val + base + (row & 31);
-                int32_t cc[TAIL_SHORT];
-                double pv[TAIL_SHORT];
-#pragma unroll
-                for (int j = 0; j < TAIL_SHORT; j++) cc[j] = j < w ? __ldg(cp + j * 32) : -1;
-#pragma unroll
-                for (int j = 0; j < TAIL_SHORT; j++)
-                    pv[j] = cc[j] >= 0 ? __dmul_rn(__ldg(vp + j * 32), __ldcg(xg + cc[j])) : 0.0;
-#pragma unroll
-                for (int j = 0; j < TAIL_SHORT; j++)
-                    if (cc[j] >= 0) y = __dadd_rn(y, pv[j]);
-            }
-            if (row < A.nrows) epi(row, y);
-        }
-        return;
-    }
-    constexpr int NW = TAIL_THREADS / 32;
-    for (int64_t s = blockIdx.x; s < A.nslices; s += gridDim.x) {
-        const int64_t row = s * 32 + lane;
-        const int64_t base = __ldg(A.slice_ptr + s);
-        const int w = (int)((__ldg(A.slice_ptr + s + 1) - base) >> 5);
-        double sum = 0.0;
-        for (int j0 = 0; j0 < w; j0 += TAIL_CHUNK) {
-            const int jn = min(TAIL_CHUNK, w - j0);
-            for (int j = warp; j < jn; j += NW * 8) {
-                int32_t cc[8];
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int jj = j + u * NW;
-                    cc[u] = jj < jn ? __ldg(A.col + base + (int64_t)(j0 + jj) * 32 + lane) : -2;
-                }
-#pragma unroll
-                for (int u = 0; u < 8; u++) {
-                    const int jj = j + u * NW;
-                    if (cc[u] == -2) continue;
-                    const double v = __ldg(A.val + base + (int64_t)(j0 + jj) * 32 + lane);
-                    prod[jj * 32 + lane] = cc[u] >= 0 ? __dmul_rn(v, __ldcg(xg + cc[u])) : 0.0;
-                }
-            }
-            __syncthreads();
-            if (warp == 0)
-                for (int j = 0; j < jn; j++) sum = __dadd_rn(sum, prod[j * 32 + lane]);
-            __syncthreads();
-        }
-        if (warp == 0 && row < A.nrows) epi(row, sum);
-    }
-}
-
-template <bool FIRST, bool LAST, bool X0>
-__device__ __forceinline__ void tail_cheb4(const TailLev &L, const double *b, const double *xg,
-                                           double *r, double *zn, double *x, int j, double *prod) {
-    const double *c = L.coef + 3 * (j - 1);
-    tail_phase(L.A, L.wA, xg, Cheb4Step<FIRST, LAST, X0>{L.m, b, xg, r, zn, x, c[0], c[1], c[2]}, prod);
-}
-
-template <bool FIRST, bool LAST, bool X0>
-__device__ __forceinline__ void tail_cheb1(const TailLev &L, const double *b, const double *xg,
-                                           double *r, double *dn, double *x, int j, double *prod) {
-    const double c0 = j == 0 ? L.coef[0] : L.coef[1 + 2 * (j - 1)];
-    const double c1 = j == 0 ? 0.0 : L.coef[2 + 2 * (j - 1)];
-    if (L.rho == 1.0)
-        tail_phase(L.A, L.wA, xg, Cheb1Step<FIRST, LAST, X0, true>{L.m, b, xg, r, dn, x, c0, c1, L.rho}, prod);
-    else
-        tail_phase(L.A, L.wA, xg, Cheb1Step<FIRST, LAST, X0, false>{L.m, b, xg, r, dn, x, c0, c1, L.rho}, prod);
-}
-
-// smoother_enqueue (smoother.cu) as grid-wide phases, same buffers and order
-__device__ void tail_smoother(const TailLev &L, const double *b, const double *x0, double *x,
-                              double *prod, cg::grid_group &grid) {
-    const int64_t n = L.n;
-    const int k = L.degree;
-    double *r = L.work, *buf[2] = {L.work + 2 * n, L.work + n}, *tmp = L.work + 3 * n;
-    const bool hx0 = x0 != nullptr;
-    if (L.family == AMGP_L1_JACOBI) {
-        const double *xin = x0;
-        for (int s = 1; s <= k; s++) {
-            double *xout = ((k - s) % 2 == 0) ? x : tmp;
-            if (s == 1 && !hx0) tail_phase(L.A, L.wA, nullptr, L1Sweep<false>{L.m, b, nullptr, xout}, prod);
-            else tail_phase(L.A, L.wA, xin, L1Sweep<true>{L.m, b, xin, xout}, prod);
-            grid.sync();
-            xin = xout;
-        }
-        return;
-    }
-    if (L.family == AMGP_CHEB4 || L.family == AMGP_OPT_CHEB4) {
-        for (int j = 1; j <= k; j++) {
-            const double *xg = (j == 1) ? x0 : buf[(j - 1) & 1];
-            double *zn = buf[j & 1];
-            if (j == 1 && k == 1) {
-                if (hx0) tail_cheb4<true, true, true>(L, b, xg, r, zn, x, j, prod);
-                else tail_cheb4<true, true, false>(L, b, xg, r, zn, x, j, prod);
-            } else if (j == 1) {
-                if (hx0) tail_cheb4<true, false, true>(L, b, xg, r, zn, x, j, prod);
-                else tail_cheb4<true, false, false>(L, b, xg, r, zn, x, j, prod);
-            } else if (j == k) {
-                tail_cheb4<false, true, false>(L, b, xg, r, zn, x, j, prod);
-            } else {
-                tail_cheb4<false, false, false>(L, b, xg, r, zn, x, j, prod);
-            }
-            grid.sync();
-        }
-        return;
-    }
-    for (int j = 0; j < k; j++) {  // opt_cheb1
-        const double *xg = (j == 0) ? x0 : buf[j & 1];
-        double *dn = buf[(j + 1) & 1];
-        const bool last = (j == k - 1);
-        if (j == 0) {
-            if (last) {
-                if (hx0) tail_cheb1<true, true, true>(L, b, xg, r, dn, x, j, prod);
-                else tail_cheb1<true, true, false>(L, b, xg, r, dn, x, j, prod);
-            } else {
-                if (hx0) tail_cheb1<true, false, true>(L, b, xg, r, dn, x, j, prod);
-                else tail_cheb1<true, false, false>(L, b, xg, r, dn, x, j, prod);
-            }
-        } else if (last) {
-            tail_cheb1<false, true, false>(L, b, xg, r, dn, x, j, prod);
-        } else {
-            tail_cheb1<false, false, false>(L, b, xg, r, dn, x, j, prod);
-        }
-        grid.sync();
-    }
-}
-
-// coarsest level: k_coarse_l1's arithmetic, run by CTA 0 in shared memory
-__device__ void tail_coarse(const TailLev &L, const double *b, double *x, int sweeps, double *sh) {
-    const SellView &A = L.A;
-    const int64_t n = A.nrows;
-    const int64_t stored = A.slice_ptr[A.nslices];
-    double *buf[2] = {sh, sh + n};
-    double *pv = sh + 2 * n;
-    double *prod = pv + stored;
-    int32_t *pc = (int32_t *)(prod + stored);
-    for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
-        pv[e] = A.val[e];
-        pc[e] = A.col[e];
-    }
-    __syncthreads();
-    for (int s = 1; s <= sweeps; s++) {
-        const double *xin = buf[(s - 1) & 1];
-        double *xout = buf[s & 1];
-        if (s > 1) {
-            for (int64_t e = threadIdx.x; e < stored; e += blockDim.x) {
-                const int32_t c = pc[e];
-                prod[e] = c >= 0 ? __dmul_rn(pv[e], xin[c]) : 0.0;
-            }
-            __syncthreads();
-        }
-        for (int64_t row = threadIdx.x; row < n; row += blockDim.x) {
-            double y = 0.0;
-            if (s > 1) {
-                const int64_t sl = row >> 5;
-                const int lane = row & 31;
-                const int64_t base = A.slice_ptr[sl];
-                const int w = (int)((A.slice_ptr[sl + 1] - base) >> 5);
-                const double *pp = prod + base + lane;
-                for (int j = 0; j < w; j++) y = __dadd_rn(y, pp[j * 32]);
-            }
-            const double rr = __dsub_rn(__ldcg(b + row), y);
-            xout[row] = __dadd_rn(s > 1 ? xin[row] : 0.0, __ddiv_rn(rr, L.m[row]));
-        }
-        __syncthreads();
-    }
-    for (int64_t row = threadIdx.x; row < n; row += blockDim.x) x[row] = buf[sweeps & 1][row];
-}
-
-__global__ void __launch_bounds__(TAIL_THREADS, 1)
-k_vcycle_tail(const TailDesc *__restrict__ D, const double *r0, double *z0) {
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ double smem[];
-    const int L = D->nlev;
-    for (int t = 0; t < L - 1; t++) {  // down: amg.py:310-312
-        const TailLev &V = D->lev[t];
-        const double *r = t == 0 ? r0 : V.r;
-        tail_smoother(V, r, nullptr, V.xpre, smem, grid);
-        tail_phase(V.A, V.wA, V.xpre, SpmvEpi<1>{r, V.res}, smem);
-        grid.sync();
-        tail_phase(V.R, V.wR, V.res, SpmvEpi<0>{nullptr, (double *)D->lev[t + 1].r}, smem);
-        grid.sync();
-    }
-    {  // coarsest: amg.py:299-300
-        const TailLev &C = D->lev[L - 1];
-        if (blockIdx.x == 0) tail_coarse(C, L == 1 ? r0 : C.r, L == 1 ? z0 : C.z, D->coarse_sweeps, smem);
-        grid.sync();
-    }
-    for (int t = L - 2; t >= 0; t--) {  // up: amg.py:314-315
-        const TailLev &V = D->lev[t];
-        const double *r = t == 0 ? r0 : V.r;
-        tail_phase(V.P, V.wP, D->lev[t + 1].z, SpmvEpi<2>{nullptr, V.xpre}, smem);
-        grid.sync();
-        tail_smoother(V, r, V.xpre, t == 0 ? z0 : V.z, smem, grid);
-    }
-}
-
-// ---------------------------------------------------------------- K8 host side
-static void tail_plan(amgp_hier *h) {
-    h->tail_start = -1;
-    if (!h->use_tail || h->coarse_solver != AMGP_COARSE_L1_JACOBI) return;
-    const int Lc = h->nlev - 1;
-    amgp_mat *C = h->A[Lc];
-    if (C->halo || tail_coarse_smem(C) > TAIL_COARSE_SMEM || C->nrows > TAIL_MAX_ROWS) return;
-    int start = Lc;
-    for (int l = Lc - 1; l >= 0 && Lc - l < TAIL_MAX_LEV; l--) {
-        const amgp_mat *A = h->A[l];
-        if (A->halo || h->P[l]->halo || h->R[l]->halo) break;
-        if (A->stored > TAIL_MAX_STORED || A->nrows > TAIL_MAX_ROWS) break;
-        if (h->plan[l].degree > TAIL_MAX_K) break;
-        start = l;
-    }
-    if (start == Lc) return;  // a coarse solve alone is already one kernel
-    h->tail_start = start;
-}
-
-static int tail_prepare(amgp_hier *h) {
-    if (!h->tail_dirty) return AMGP_OK;
-    tail_plan(h);
-    h->tail_dirty = false;
-    if (h->tail_start < 0) return AMGP_OK;
-    TailDesc d;
-    memset(&d, 0, sizeof(d));
-    d.nlev = h->nlev - h->tail_start;
-    d.coarse_sweeps = h->coarse_sweeps;
-    for (int t = 0; t < d.nlev; t++) {
-        const int l = h->tail_start + t;
-        TailLev &V = d.lev[t];
-        V.A = view_of(h->A[l]);
-        V.wA = h->A[l]->max_width;
-        if (l < h->nlev - 1) {
-            V.P = view_of(h->P[l]);
-            V.R = view_of(h->R[l]);
-            V.wP = h->P[l]->max_width;
-            V.wR = h->R[l]->max_width;
-        }
-        V.m = h->m[l];
-        V.r = h->rl[l];
-        V.z = h->zl[l];
-        V.xpre = h->xpre[l];
-        V.res = h->res[l];
-        V.work = h->work[l];
-        V.n = h->A[l]->nrows;
-        const SmootherPlan &p = (l == h->nlev - 1) ? h->coarse_plan : h->plan[l];
-        V.family = p.family;
-        V.degree = p.degree;
-        V.rho = p.rho;
-        std::copy(p.coef.begin(), p.coef.begin() + std::min<size_t>(p.coef.size(), 3 * TAIL_MAX_K), V.coef);
-    }
-    if (!h->d_tail) AMGP_CUDA(cudaMalloc(&h->d_tail, sizeof(TailDesc)));
-    AMGP_CUDA(cudaStreamSynchronize(h->ctx->stream));
-    AMGP_CUDA(cudaMemcpy(h->d_tail, &d, sizeof(TailDesc), cudaMemcpyHostToDevice));
-    h->tail_smem = std::max<size_t>((size_t)TAIL_CHUNK * 32 * sizeof(double), tail_coarse_smem(h->A[h->nlev - 1]));
-    AMGP_CUDA(cudaFuncSetAttribute(k_vcycle_tail, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)h->tail_smem));
-    int per_sm = 0, nsm = 0;
-    AMGP_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_vcycle_tail, TAIL_THREADS,
-                                                            h->tail_smem));
-    AMGP_CUDA(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, h->ctx->device));
-    if (per_sm < 1) {
-        h->tail_start = -1;
-        return AMGP_OK;
-    }
-    h->tail_grid = nsm;  // one CTA per SM
-    return AMGP_OK;
-}
-
-static int tail_enqueue(amgp_hier *h, const double *r, double *z) {
-    amgp_ctx *ctx = h->ctx;
-    const TailDesc *d = h->d_tail;
-    void *args[] = {(void *)&d, (void *)&r, (void *)&z};
-    AMGP_CUDA(cudaLaunchCooperativeKernel((const void *)k_vcycle_tail, dim3(h->tail_grid),
-                                          dim3(TAIL_THREADS), args, h->tail_smem, ctx->stream));
-    ctx->launches.fetch_add(1);
-    return AMGP_OK;
-}
-
 static int vcycle_level(amgp_hier *h, int l, const double *r, double *z) {
-    if (l == h->tail_start) return tail_enqueue(h, r, z);
     if (l == h->nlev - 1) return coarse_enqueue(h, r, z);
     amgp_ctx *ctx = h->ctx;
     amgp_mat *A = h->A[l];
@@ -571,13 +222,6 @@ static int vcycle_level(amgp_hier *h, int l, const double *r, double *z) {
 // Enqueue one V-cycle (graph replay when enabled).  Caller holds h->mu.
 int vcycle_enqueue(amgp_hier *h, const double *r, double *z) {
     amgp_ctx *ctx = h->ctx;
-    if (h->tail_dirty) {  // (re)plan the cooperative tail before any capture
-        if (h->gexec) {
-            cudaGraphExecDestroy(h->gexec);
-            h->gexec = nullptr;
-        }
-        AMGP_TRY(tail_prepare(h));
-    }
     if (!h->use_graph) return vcycle_level(h, 0, r, z);
     if (!h->gexec || h->g_r != r || h->g_z != z) {
         if (h->gexec) {
@@ -615,7 +259,6 @@ static void hier_free_buffers(amgp_hier *h) {
     for (auto *v : {&h->rl, &h->zl, &h->xpre, &h->res, &h->work})
         for (double *p : *v) cudaFree(p);
     cudaFree(h->cholL);
-    cudaFree(h->d_tail);
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
 }
 
@@ -693,7 +336,6 @@ extern "C" int amgp_hier_set_smoother(amgp_hier *h, int level, const amgp_smooth
     if (level >= h->nlev) return amgp_fail(AMGP_EINVAL, "level out of range");
     for (int l = 0; l < h->nlev; l++)
         if (level < 0 || l == level) h->plan[l] = p;
-    h->tail_dirty = true;
     if (h->gexec) {  // invalidate the captured graph
         cudaStreamSynchronize(h->ctx->stream);
         cudaGraphExecDestroy(h->gexec);
@@ -713,7 +355,6 @@ extern "C" int amgp_hier_set_coarse_cholesky(amgp_hier *h, const double *L) {
     AMGP_CUDA(cudaMalloc(&h->cholL, std::max<int64_t>(n * n, 1) * sizeof(double)));
     AMGP_CUDA(cudaMemcpy(h->cholL, L, n * n * sizeof(double), cudaMemcpyHostToDevice));
     h->coarse_solver = AMGP_COARSE_DENSE_DIRECT;
-    h->tail_dirty = true;
     if (h->gexec) {
         cudaGraphExecDestroy(h->gexec);
         h->gexec = nullptr;
@@ -728,20 +369,9 @@ extern "C" int amgp_hier_use_graph(amgp_hier *h, int enable) {
     return AMGP_OK;
 }
 
-extern "C" int amgp_hier_use_tail(amgp_hier *h, int enable) {
+extern "C" int amgp_hier_info(amgp_hier *h, int *nlevels) {
     if (!h) return amgp_fail(AMGP_EINVAL, "null hierarchy");
-    std::lock_guard<std::mutex> g(h->mu);
-    h->use_tail = enable != 0;
-    h->tail_dirty = true;
-    return AMGP_OK;
-}
-
-extern "C" int amgp_hier_info(amgp_hier *h, int *nlevels, int *tail_start) {
-    if (!h) return amgp_fail(AMGP_EINVAL, "null hierarchy");
-    std::lock_guard<std::mutex> g(h->mu);
-    if (h->tail_dirty) AMGP_TRY(tail_prepare(h));
     if (nlevels) *nlevels = h->nlev;
-    if (tail_start) *tail_start = h->tail_start;
     return AMGP_OK;
 }
 

@@ -3,8 +3,7 @@
 Bitwise smoother apply on generated row blocks and bitwise V-cycles of a
 row-partitioned native hierarchy against the C oracle; distributed PCG/FCG
 iteration counts equal to the oracle's (+-1 bar) -- for each halo transport:
-NCCL send/recv, the direct NVLink transport (default), and its fused
-single-launch variant.
+NCCL send/recv and the direct NVLink transport (default).
 """
 
 import json
@@ -46,10 +45,7 @@ def run_dist_check(nproc, grid, graph, transport):
     if graph:
         cmd.append("--graph")
     env = dict(os.environ)
-    env.pop("AMGP_P2P_FUSED", None)
     env["AMGP_HALO"] = "nccl" if transport == "nccl" else "p2p"
-    if transport == "p2p_fused":  # one launch: pack CTAs + interior + boundary (halo double-buffered)
-        env["AMGP_P2P_FUSED"] = "1"
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env)
     lines = [json.loads(l) for l in p.stdout.splitlines() if l.startswith("{")]
     assert len(lines) == nproc, p.stdout[-2000:] + p.stderr[-2000:]
@@ -58,7 +54,7 @@ def run_dist_check(nproc, grid, graph, transport):
     assert p.returncode == 0
 
 
-@pytest.mark.parametrize("transport", ["nccl", "p2p", "p2p_fused"])
+@pytest.mark.parametrize("transport", ["nccl", "p2p"])
 @pytest.mark.parametrize("graph", [False, True])
 def test_dist_check_two_gpus(graph, transport):
     # 24^3: every distributed matrix has < 2 slices per SM per rank -> the

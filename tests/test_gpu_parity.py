@@ -198,36 +198,6 @@ def test_vcycle_bitwise_vs_reference(P, prefix):
             assert np.array_equal(P.vcycle_apply(h, r), d[f"{prefix}_vc_{fam}_k{k}"]), (fam, k)
 
 
-@pytest.mark.parametrize("m,kind", [(16, "smoothed_aggregation"), (32, "smoothed_aggregation"),
-                                    (32, "pairwise_matching"), (48, "smoothed_aggregation")])
-def test_cooperative_tail_is_bitwise_identical(P, m, kind):
-    """K8 (whole bottom of the V-cycle in one cooperative kernel) gives the
-    same bits as per-step launches, graph and eager, all families."""
-    A, _ = P.poisson3d(m)
-    h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=kind),
-                          smoother=P.PolySmootherConfig(family="cheb4", degree=4))
-    D = h.device()
-    r = np.random.default_rng(7).standard_normal(A.nrows)
-    D.use_tail(True)
-    if D.tail_start() < 0:
-        pytest.skip("no level qualifies for the cooperative tail")
-    for fam in FAMILIES:
-        for k in (1, 3, 4):
-            cfg = P.PolySmootherConfig(family=fam, degree=k)
-            for lv in h.levels:
-                lv.smoother = cfg
-            outs = []
-            for tail in (True, False):
-                for graph in (True, False):
-                    D.use_tail(tail)
-                    D.use_graph(graph)
-                    outs.append(P.vcycle_apply(h, r))
-            for o in outs[1:]:
-                assert np.array_equal(o, outs[0]), (fam, k)
-    D.use_tail(False)
-    D.use_graph(True)
-
-
 def test_vcycle_zero_and_linearity(P, rng):
     h, d = golden_hierarchy(P, "sa16", P.PolySmootherConfig(family="opt_cheb1", degree=4))
     n = h.levels[0].A.nrows

@@ -22,14 +22,13 @@ def main():
     ap.add_argument("--k", type=int, default=4)
     ap.add_argument("--repeat", type=int, default=2)
     ap.add_argument("--no-graph", action="store_true")
-    ap.add_argument("--tail", action="store_true", help="enable the cooperative V-cycle tail")
     args = ap.parse_args()
     import torch
 
     import paper_2407_09848_b200 as P
     from paper_2407_09848_b200 import _native as N
 
-    A, b = (P.poisson3d if args.stencil == 7 else P.poisson3d_27)(args.m)
+    A = P.poisson3d_device(args.m, args.stencil)
     t0 = time.perf_counter()
     h = P.build_hierarchy(A, coarsening=P.CoarseningConfig(kind=args.kind),
                           smoother=P.PolySmootherConfig(family=args.family, degree=args.k))
@@ -37,15 +36,13 @@ def main():
     D = h.device()
     if args.no_graph:
         D.use_graph(False)
-    if args.tail:
-        D.use_tail(True)
     bd = torch.ones(A.nrows, dtype=torch.float64, device="cuda")
     for i in range(args.repeat):
         x, rep = P.solve(A, bd, precond=P.as_vcycle_preconditioner(h), cfg=P.KrylovConfig(tol=1e-6))
         torch.cuda.synchronize()
         print(f"m={args.m} {args.stencil}-pt {args.kind} {args.family} k={args.k}: setup {setup:.2f}s "
               f"iters {rep.iterations} relres {rep.final_relres:.3e} solve {rep.elapsed_s * 1e3:.2f} ms "
-              f"levels {[lv.A.nrows for lv in h.levels]} tail_start {D.tail_start()}", flush=True)
+              f"levels {[lv.A.nrows for lv in h.levels]}", flush=True)
 
 
 if __name__ == "__main__":

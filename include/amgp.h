@@ -120,6 +120,15 @@ int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
                         const amgp_smoother_cfg *cfg, const double *b, const double *x0,
                         double *x);
 
+/* smoother_apply over HOST buffers, napply independent applications
+ * (cfgs[i], b_host[i], x0_host[i] (NULL: zero guess) -> x_host[i]); uploads,
+ * kernels and downloads of consecutive applications overlap (two device
+ * slots, two copy streams, full-duplex PCIe); returns when every x_host[i]
+ * is written.  Results equal amgp_smoother_apply's bit for bit. */
+int amgp_smoother_apply_host(amgp_ctx *ctx, amgp_mat *A, const double *m, int napply,
+                             const amgp_smoother_cfg *cfgs, const double *const *b_host,
+                             const double *const *x0_host, double *const *x_host);
+
 /* ---- V-cycle (amg.py:47-91, 293-319) ----------------------------------- */
 /* Levels fine->coarse: A[l], m[l] (device l1 diagonals), P[l] (n_l x n_{l+1})
  * and R[l] = P[l]^T (amg.py:56-59) for l < nlevels-1.  The hierarchy keeps

@@ -27,6 +27,7 @@ from .smoothers import (
     as_preconditioner,
     l1_jacobi_diag,
     smoother_apply,
+    smoother_apply_batch,
     smoother_error_apply,
 )
 from .sparse import CsrMatrix, DeviceMatrix, fused_update, reset_spmv_count, spmv, spmv_count

@@ -72,6 +72,8 @@ struct amgp_ctx {
     // and synchronisation words mapped through CUDA IPC; the kernels
     // themselves signal and wait (sync_stride words per matrix slot)
     int halo_p2p = 0;  // 0: NCCL, 1: p2p (default)
+    // copy streams of the host-buffer smoother path (created on first use)
+    cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
     unsigned long long *sync = nullptr;            // [AMGP_MAX_SLOTS][sync_stride]
     std::vector<unsigned long long *> peer_sync;   // every rank's sync array (self included)
     int sync_stride = 0;
@@ -136,6 +138,9 @@ struct amgp_mat {
     // per-matrix smoother workspace (r, two operand buffers, x copy)
     double *work = nullptr;
     int64_t work_n = 0;
+    // host-buffer path (amgp_smoother_apply_host): two (b, x0, x) slots
+    double *io = nullptr;
+    int64_t io_n = 0;
     std::mutex mu;
 };
 

@@ -67,6 +67,8 @@ int amgp_ctx_destroy(amgp_ctx *c) {
     cudaFree(c->scalars);
     cudaFreeHost(c->host_scalars);
     if (c->own_stream) cudaStreamDestroy(c->stream);
+    if (c->io_h2d) cudaStreamDestroy(c->io_h2d);
+    if (c->io_d2h) cudaStreamDestroy(c->io_d2h);
     delete c;
     return AMGP_OK;
 }

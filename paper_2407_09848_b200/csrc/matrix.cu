@@ -134,6 +134,7 @@ extern "C" int amgp_mat_destroy(amgp_mat *A) {
     cudaFree(A->col);
     cudaFree(A->val);
     cudaFree(A->work);
+    cudaFree(A->io);
     delete A;
     return AMGP_OK;
 }

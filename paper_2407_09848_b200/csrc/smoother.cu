@@ -197,6 +197,83 @@ extern "C" int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
     return smoother_enqueue(ctx, A, m, p, b, x0, x, A->work);
 }
 
+// End-to-end path with host buffers (the reference-facing call for host
+// data): napply independent applications, apply i reading b_host[i] and
+// x0_host[i] (NULL: zero guess) and writing x_host[i].  Two device slots and
+// two copy streams pipeline the calls: the upload of apply i+1 and the
+// download of apply i-1 run while apply i's kernels stream the matrix, and
+// PCIe carries H2D and D2H at once (full duplex).  Pinned host buffers give
+// asynchronous DMA; pageable ones still work (the driver stages them).
+// Every apply computes exactly what amgp_smoother_apply computes.
+extern "C" int amgp_smoother_apply_host(amgp_ctx *ctx, amgp_mat *A, const double *m, int napply,
+                                        const amgp_smoother_cfg *cfgs, const double *const *b_host,
+                                        const double *const *x0_host, double *const *x_host) {
+    if (!ctx || !A || napply < 0 || (napply && (!cfgs || !b_host || !x_host)))
+        return amgp_fail(AMGP_EINVAL, "amgp_smoother_apply_host: bad argument");
+    if (A->nrows != (A->halo ? A->halo->nown : A->ncols)) return amgp_fail(AMGP_EINVAL, "dimension mismatch");
+    const int64_t n = A->nrows;
+    if (n > 0 && !m) return amgp_fail(AMGP_EINVAL, "null vector");
+    std::vector<SmootherPlan> plans(napply);
+    for (int i = 0; i < napply; i++) {
+        AMGP_TRY(make_smoother_plan(&cfgs[i], &plans[i]));
+        if (n > 0 && (!b_host[i] || !x_host[i])) return amgp_fail(AMGP_EINVAL, "null vector");
+    }
+    if (napply == 0 || n == 0) return AMGP_OK;
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> g(A->mu);
+    AMGP_TRY(ensure_work(A, smoother_work_doubles(n) + n));
+    if (A->io_n < 6 * n) {  // two slots of (b, x0, x)
+        cudaStreamSynchronize(ctx->stream);
+        cudaFree(A->io);
+        A->io = nullptr;
+        A->io_n = 0;
+        AMGP_CUDA(cudaMalloc(&A->io, (size_t)6 * n * sizeof(double)));
+        A->io_n = 6 * n;
+    }
+    {
+        std::lock_guard<std::mutex> cg(ctx->mu);
+        if (!ctx->io_h2d) AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->io_h2d, cudaStreamNonBlocking));
+        if (!ctx->io_d2h) AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->io_d2h, cudaStreamNonBlocking));
+    }
+    const size_t bytes = (size_t)n * sizeof(double);
+    double *db[2] = {A->io, A->io + 3 * n}, *dx0[2] = {A->io + n, A->io + 4 * n},
+           *dx[2] = {A->io + 2 * n, A->io + 5 * n};
+    cudaEvent_t ev[4][2] = {};  // in, computed, downloaded, start
+    int st = AMGP_OK;
+    for (auto &row : ev)
+        for (auto &e : row)
+            if (st == AMGP_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
+                st = amgp_cuda_fail(cudaGetLastError(), "cudaEventCreate", __FILE__, __LINE__);
+    cudaStream_t h2d = ctx->io_h2d, d2h = ctx->io_d2h, cs = ctx->stream;
+    auto chk = [&](cudaError_t e, const char *what) {
+        if (e != cudaSuccess && st == AMGP_OK) st = amgp_cuda_fail(e, what, __FILE__, __LINE__);
+    };
+    // the copies must also follow work the caller queued on the compute stream
+    chk(cudaEventRecord(ev[3][0], cs), "record");
+    chk(cudaStreamWaitEvent(h2d, ev[3][0], 0), "wait");
+    for (int i = 0; i < napply && st == AMGP_OK; i++) {
+        const int s = i & 1;
+        const bool hx0 = x0_host && x0_host[i];
+        if (i >= 2) chk(cudaStreamWaitEvent(h2d, ev[1][s], 0), "wait");  // slot's inputs consumed
+        chk(cudaMemcpyAsync(db[s], b_host[i], bytes, cudaMemcpyHostToDevice, h2d), "upload b");
+        if (hx0) chk(cudaMemcpyAsync(dx0[s], x0_host[i], bytes, cudaMemcpyHostToDevice, h2d), "upload x0");
+        chk(cudaEventRecord(ev[0][s], h2d), "record");
+        chk(cudaStreamWaitEvent(cs, ev[0][s], 0), "wait");
+        if (i >= 2) chk(cudaStreamWaitEvent(cs, ev[2][s], 0), "wait");  // slot's output downloaded
+        if (st == AMGP_OK) st = smoother_enqueue(ctx, A, m, plans[i], db[s], hx0 ? dx0[s] : nullptr, dx[s], A->work);
+        chk(cudaEventRecord(ev[1][s], cs), "record");
+        chk(cudaStreamWaitEvent(d2h, ev[1][s], 0), "wait");
+        chk(cudaMemcpyAsync(x_host[i], dx[s], bytes, cudaMemcpyDeviceToHost, d2h), "download x");
+        chk(cudaEventRecord(ev[2][s], d2h), "record");
+    }
+    chk(cudaStreamSynchronize(d2h), "sync");
+    chk(cudaStreamSynchronize(h2d), "sync");
+    for (auto &row : ev)
+        for (auto &e : row)
+            if (e) cudaEventDestroy(e);
+    return st;
+}
+
 extern "C" int amgp_fused_update(amgp_ctx *ctx, int64_t n, double rho, double rho_prev, double c,
                                  const double *s, double *r, double *d, double *x) {
     if (!ctx || n < 0) return amgp_fail(AMGP_EINVAL, "fused_update: vector length mismatch");

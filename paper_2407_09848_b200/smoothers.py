@@ -151,6 +151,79 @@ def smoother_apply(config, A, M, b, x0):
     return N.like(out, b)
 
 
+def _host_ptr(a):
+    """(ctypes pointer, keep-alive) of a host float64 vector (numpy or CPU tensor)."""
+    if N.is_torch(a):
+        if a.is_cuda or a.dtype != _torch_f64() or not a.is_contiguous():
+            raise TypeError("smoother_apply_batch: host float64 contiguous vectors expected")
+        return N._VP(a.data_ptr()), a
+    arr = np.ascontiguousarray(np.asarray(a, dtype=np.float64))
+    return N._VP(arr.ctypes.data), arr
+
+
+def _torch_f64():
+    import torch
+
+    return torch.float64
+
+
+def smoother_apply_batch(configs, A, M, bs, x0s, out=None):
+    """``smoother_apply`` for a batch of independent host-side problems
+    (configs[i], bs[i], x0s[i]) -> list of new host vectors, in one library
+    call (amgp_smoother_apply_host): the uploads, kernels and downloads of
+    consecutive applications overlap.  Each result equals
+    ``smoother_apply(configs[i], A, M, bs[i], x0s[i])`` bit for bit.  Pinned
+    torch inputs get pinned outputs (asynchronous DMA); numpy in, numpy out.
+    ``out``: optional preallocated outputs (same container types)."""
+    import ctypes
+
+    D = device_of(A)
+    k = len(configs)
+    if not (len(bs) == len(x0s) == k) or (out is not None and len(out) != k):
+        raise ValueError("smoother_apply_batch: configs, bs, x0s (and out) must have equal lengths")
+    n = D.nrows
+    keep, bp, xp, op = [], [], [], []
+    outs = []
+    for i in range(k):
+        nb = bs[i].shape[0] if hasattr(bs[i], "shape") else len(bs[i])
+        nx = x0s[i].shape[0] if hasattr(x0s[i], "shape") else len(x0s[i])
+        if nb != nx or nb != n:
+            raise ValueError("dimension mismatch")
+        p, ref = _host_ptr(bs[i])
+        keep.append(ref)
+        bp.append(p)
+        if _is_zero_host(x0s[i]):
+            xp.append(None)
+        else:
+            p, ref = _host_ptr(x0s[i])
+            keep.append(ref)
+            xp.append(p)
+        if out is not None:
+            o = out[i]
+        elif N.is_torch(bs[i]):
+            import torch
+
+            o = torch.empty(n, dtype=torch.float64, pin_memory=bs[i].is_pinned())
+        else:
+            o = np.empty(n)
+        p, ref = _host_ptr(o)
+        if ref is not o:
+            raise TypeError("smoother_apply_batch: outputs must be contiguous float64 host vectors")
+        op.append(p)
+        outs.append(o)
+    cfgs = [N.smoother_cfg(cfg) for cfg in configs]
+    carr = (N.SmootherCfg * max(k, 1))(*cfgs)
+    c = D.ctx
+    with c.scope():
+        md = _m_device(M, c)
+        N.check(N.lib().amgp_smoother_apply_host(c.handle, D.handle, N.ptr(md), k, carr,
+                                                 (N._VP * max(k, 1))(*bp), (N._VP * max(k, 1))(*xp),
+                                                 (N._VP * max(k, 1))(*op)))
+    _count(sum(int(cfg.degree) for cfg in configs))
+    del keep, ctypes
+    return outs
+
+
 def C_byref(cfg):
     import ctypes
 

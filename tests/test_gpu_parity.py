@@ -502,3 +502,29 @@ def test_coarse_solve_shared_memory_variants_bitwise(P, nc, band):
               {"A": (C1.row_ptr, C1.col_idx, C1.values), "m": m1}]
         want = oracle.Hierarchy(ol, fam, k, a=a, beta=beta).vcycle(r)
         assert np.array_equal(got, want), fam
+
+
+def test_smoother_apply_batch_host_buffers_bitwise(P):
+    """The pipelined host-buffer path (amgp_smoother_apply_host, the e2e
+    bench call) returns exactly what the per-call smoother_apply returns."""
+    import torch
+
+    A, _ = P.poisson3d(24)
+    M = P.l1_jacobi_diag(A)
+    rng = np.random.default_rng(11)
+    cfgs = [P.PolySmootherConfig(family=f, degree=k) for f in FAMILIES for k in (1, 3, 4)]
+    bs = [rng.standard_normal(A.nrows) for _ in cfgs]
+    x0s = [rng.standard_normal(A.nrows) if i % 3 else np.zeros(A.nrows) for i in range(len(cfgs))]
+    got = P.smoother_apply_batch(cfgs, A, M, bs, x0s)
+    for cfg, b, x0, g in zip(cfgs, bs, x0s, got):
+        assert np.array_equal(g, P.smoother_apply(cfg, A, M, b, x0)), cfg
+    # pinned torch buffers in, pinned out, preallocated outputs
+    bt = [torch.as_tensor(b).pin_memory() for b in bs[:4]]
+    xt = [torch.as_tensor(x).pin_memory() for x in x0s[:4]]
+    outs = [torch.empty(A.nrows, dtype=torch.float64).pin_memory() for _ in range(4)]
+    res = P.smoother_apply_batch(cfgs[:4], A, M, bt, xt, out=outs)
+    assert all(r is o for r, o in zip(res, outs))
+    for cfg, b, x0, g in zip(cfgs[:4], bs, x0s, res):
+        assert np.array_equal(g.numpy(), P.smoother_apply(cfg, A, M, b, x0))
+    with pytest.raises(ValueError):
+        P.smoother_apply_batch(cfgs[:2], A, M, bs[:1], x0s[:2])

@@ -367,7 +367,8 @@ def solve_bench(m, kind="smoothed_aggregation", cpu=True, stencil=7, k=4, cpu_fa
     return out
 
 
-def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, strong=False, replicate_below=20000):
+def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, strong=False, replicate_below=20000,
+                     variant="pcg"):
     """PCG + AMG solve over all ranks (also N = 1): weak-scaled (BASELINE
     configs[3]: global cube round(m_base N^(1/3)), ~m_base^3 rows per GPU) or
     strong-scaled (configs[4]: global cube m_base).  Each rank generates its
@@ -408,7 +409,7 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, stron
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         setup_s = float(t.item())
     bd = torch.ones(hi - lo, dtype=torch.float64, device="cuda")
-    kc = P.KrylovConfig(tol=1e-6, itmax=1000)
+    kc = P.KrylovConfig(tol=1e-6, itmax=1000, variant=variant)
 
     def run():
         if dh is not None:
@@ -438,7 +439,8 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, stron
             "distributed_levels": sum(p is not None for p in dh.parts) if dh is not None else 0,
             "setup": "device" + (", distributed (decoupled aggregation)" if comm is not None else ""),
             "setup_s": setup_s, "iterations": rep.iterations, "final_relres": rep.final_relres,
-            "solve_s": sec, "wall_s": float(t[1].item()), "tol": 1e-6,
+            "solve_s": sec, "wall_s": float(t[1].item()), "tol": 1e-6, "krylov": variant,
+            "replicate_below": replicate_below,
             "roofline_rank0": solve_roofline(shapes, k, family, rep.iterations, sec, peak)}
 
 
@@ -465,7 +467,8 @@ def run_b200(args):
 
             comm = Dist.Communicator(local)
         res = dist_solve_bench(comm, args.weak_grid, ws, family=args.solve_family or "opt_cheb4",
-                               k=args.solve_k, stencil=args.solve_stencil, strong=args.solve_scaling == "strong")
+                               k=args.solve_k, stencil=args.solve_stencil, strong=args.solve_scaling == "strong",
+                               replicate_below=args.replicate_below, variant=args.krylov)
         if rank == 0:
             res["peak_mem_gb_rank0"] = torch.cuda.max_memory_allocated() / 1e9
             print(json.dumps({"solve_only": True, "n_gpus": ws, "solve": res}), flush=True)
@@ -654,6 +657,10 @@ def main():
     ap.add_argument("--solve-family", default=None,
                     help="smoother family of the multi-GPU solve / the CPU oracle solve "
                          "(default opt_cheb4 / opt_cheb1)")
+    ap.add_argument("--replicate-below", type=int, default=20000,
+                    help="N > 1: AMG levels with fewer global rows are replicated on every rank")
+    ap.add_argument("--krylov", default="pcg", choices=["pcg", "fcg", "pcg1"],
+                    help="Krylov variant of the multi-GPU / weak-scaling solves")
     ap.add_argument("--solve-only", action="store_true",
                     help="run only the --weak-grid solve (diagnostics for BASELINE configs[3]/[4])")
     ap.add_argument("--solve-scaling", default="weak", choices=["weak", "strong"],

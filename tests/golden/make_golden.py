@@ -352,6 +352,16 @@ def big():
     print("wrote", path)
 
 
+def a_star_beyond_table():
+    """a*_k solved by the reference for degrees past its table (optimize.py:313-318)."""
+    from amgpoly.optimize import solve_a_star
+
+    doc = {str(k): solve_a_star(k) for k in range(21, 41)}
+    with open(os.path.join(HERE, "a_star_k21_40.json"), "w") as f:
+        json.dump(doc, f, indent=1)
+    print("wrote a_star_k21_40.json")
+
+
 def cli_reports():
     """Reference `amgpoly solve` JSON reports (cli.py:193-255) for small runs."""
     from amgpoly.cli import main as cli_main
@@ -369,6 +379,9 @@ def cli_reports():
 if __name__ == "__main__":
     if sys.argv[1:] == ["big"]:
         big()
+        sys.exit(0)
+    if sys.argv[1:] == ["a_star"]:
+        a_star_beyond_table()
         sys.exit(0)
     export_params()
     smoother_small()

@@ -211,3 +211,21 @@ def test_device_ops_fail_loudly_without_gpu():
     cfg = P.PolySmootherConfig(family="cheb4", degree=2)
     with pytest.raises(RuntimeError, match="CUDA device"):
         P.smoother_apply(cfg, A, P.l1_jacobi_diag(A), b, np.zeros_like(b))
+
+
+def test_optimal_a_beyond_the_table_matches_reference():
+    """optimal_a(k) for k > 20 solves for a*_k (reference optimize.py:106-111,
+    313-318) with the same bits as the reference's solver; the restated Brent
+    iteration also reproduces the shipped k <= 20 table exactly."""
+    import json
+
+    from paper_2407_09848_b200 import params as Pm
+
+    ref = golden("a_star_k21_40.json")
+    for k, v in ref.items():
+        assert Pm.optimal_a(int(k)) == v, k
+    table = json.load(open(os.path.join(REPO, "paper_2407_09848_b200", "data", "smoother_params.json")))["a_star"]
+    for k, v in table.items():
+        assert Pm.solve_a_star(int(k)) == float(v), k
+    with pytest.raises(ValueError):
+        Pm.solve_a_star(0)

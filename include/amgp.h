@@ -120,6 +120,11 @@ int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
                         const amgp_smoother_cfg *cfg, const double *b, const double *x0,
                         double *x);
 
+/* out = a + s*b (sign > 0) or a - s*b (sign < 0), the product rounded
+ * first: numpy's axpy expressions of krylov.py:101-119 (the PCG of a solve
+ * whose preconditioner is a user callable). */
+int amgp_vec_update(amgp_ctx *ctx, int64_t n, double s, const double *a, const double *b, double *out,
+                    int sign);
 /* smoother_apply over HOST buffers, napply independent applications
  * (cfgs[i], b_host[i], x0_host[i] (NULL: zero guess) -> x_host[i]); uploads,
  * kernels and downloads of consecutive applications overlap (two device

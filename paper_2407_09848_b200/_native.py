@@ -80,6 +80,7 @@ _SIGS = {
     "amgp_fused_update": (C.c_int, [_VP, C.c_int64, C.c_double, C.c_double, C.c_double,
                                      _VP, _VP, _VP, _VP]),
     "amgp_smoother_apply": (C.c_int, [_VP, _VP, _VP, C.POINTER(SmootherCfg), _VP, _VP, _VP]),
+    "amgp_vec_update": (C.c_int, [_VP, C.c_int64, C.c_double, _VP, _VP, _VP, C.c_int]),
     "amgp_smoother_apply_host": (C.c_int, [_VP, _VP, _VP, C.c_int, C.POINTER(SmootherCfg), C.POINTER(_VP),
                                            C.POINTER(_VP), C.POINTER(_VP)]),
     "amgp_hier_create": (C.c_int, [_VP, C.c_int, C.POINTER(_VP), C.POINTER(_VP), C.POINTER(_VP),

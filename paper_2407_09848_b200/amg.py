@@ -66,7 +66,9 @@ class DeviceHierarchy:
         self.levels = h.levels
         L = len(h.levels)
         self._A = [device_of(lv.A) for lv in h.levels]
-        self._m = [lv.M.device(c) for lv in h.levels]
+        from .smoothers import _m_device
+
+        self._m = [_m_device(lv.M, c) for lv in h.levels]
         self._P = [device_of(lv.P) for lv in h.levels[:-1]]
         self._R = [device_of(lv.restrict_op()) for lv in h.levels[:-1]]
         Aa = (N._VP * L)(*[a.handle for a in self._A])
@@ -206,19 +208,62 @@ def _gpu_present():
         return False
 
 
+class _TailView:
+    """Levels _level.. of a hierarchy as a hierarchy of their own (a V-cycle
+    started below the finest level, reference amg.py:303 with _level > 0)."""
+
+    def __init__(self, h, level):
+        self.levels = h.levels[level:]
+        self.coarse_solver = h.coarse_solver
+        self.coarse_sweeps = h.coarse_sweeps
+
+
+def _device_hierarchy(h, level=0):
+    """DeviceHierarchy of ours (h.device()) or of any object with the
+    reference AmgHierarchy fields (levels of A, M, smoother, P and
+    restrict_op(); coarse_solver, coarse_sweeps), built once and cached."""
+    if level == 0 and isinstance(h, AmgHierarchy):
+        return h.device()
+    cache = getattr(h, "_b200_devs", None)
+    if cache is None:
+        cache = {}
+        try:
+            h._b200_devs = cache
+        except AttributeError:
+            pass
+    if level not in cache:
+        cache[level] = DeviceHierarchy(_TailView(h, level) if level else h)
+    return cache[level]
+
+
+def vcycle_spmv_count(h, level=0):
+    """SpMVs one reference V-cycle performs from `level` (cost accounting of
+    sparse.py:18-29): per level pre + post smoother degrees, residual,
+    restriction, prolongation; coarse l1 sweeps (dense_direct: none)."""
+    n = 0
+    L = len(h.levels)
+    for l in range(level, L - 1):
+        n += 2 * h.levels[l].smoother.degree + 3
+    if h.coarse_solver != "dense_direct":
+        n += h.coarse_sweeps
+    return n
+
+
 def vcycle_apply(h, r, _level=0):
-    """One symmetric V-cycle applied to a residual on the GPU; returns the correction."""
+    """One symmetric V-cycle applied to a residual on the GPU; returns the
+    correction (amg.py:303-315).  h: our hierarchy or the reference's."""
     n = r.shape[0] if hasattr(r, "shape") else len(r)
     if n != h.levels[_level].A.nrows:
         raise ValueError("dimension mismatch")
-    if _level != 0:
-        raise ValueError("device V-cycle starts at the finest level")
-    D = h.device()
+    D = _device_hierarchy(h, _level)
     c = D.ctx
     with c.scope():
         rd = N.to_device(r, c)
         z = N.empty(n, c)
         D.apply(rd, z)
+    from .sparse import _count
+
+    _count(vcycle_spmv_count(h, _level))
     return N.like(z, r)
 
 

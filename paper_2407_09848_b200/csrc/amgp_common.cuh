@@ -54,7 +54,10 @@ struct amgp_ctx {
     cudaStream_t stream = nullptr;
     bool own_stream = false;
     std::atomic<int64_t> launches{0};
-    std::mutex mu;  // serialises API calls that share ctx scratch
+    // Serialises the API calls that enqueue work: they share this stream,
+    // and a V-cycle graph capture must not see another thread's launches
+    // (lock order: ctx->mu, then a matrix's or hierarchy's own mutex).
+    std::mutex mu;
     // deterministic-reduction scratch (PCG): partial sums + scalars
     double *red_partial = nullptr;
     int64_t red_partial_n = 0;

@@ -410,5 +410,6 @@ extern "C" int amgp_spmv(amgp_ctx *ctx, const amgp_mat *A, const double *x, doub
     if (!ctx || !A || (!x && A->ncols) || (!y && A->nrows))
         return amgp_fail(AMGP_EINVAL, "amgp_spmv: bad argument");
     AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> cg(ctx->mu);
     return spmv_enqueue(ctx, A, x, y);
 }

@@ -186,6 +186,7 @@ extern "C" int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
     SmootherPlan p;
     AMGP_TRY(make_smoother_plan(cfg, &p));
     AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> cg(ctx->mu);  // API calls share the context stream (see amgp_common.cuh)
     std::lock_guard<std::mutex> g(A->mu);
     const int64_t n = A->nrows;
     AMGP_TRY(ensure_work(A, smoother_work_doubles(n) + n));
@@ -220,6 +221,7 @@ extern "C" int amgp_smoother_apply_host(amgp_ctx *ctx, amgp_mat *A, const double
     }
     if (napply == 0 || n == 0) return AMGP_OK;
     AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> cg(ctx->mu);
     std::lock_guard<std::mutex> g(A->mu);
     AMGP_TRY(ensure_work(A, smoother_work_doubles(n) + n));
     if (A->io_n < 6 * n) {  // two slots of (b, x0, x)
@@ -230,11 +232,8 @@ extern "C" int amgp_smoother_apply_host(amgp_ctx *ctx, amgp_mat *A, const double
         AMGP_CUDA(cudaMalloc(&A->io, (size_t)6 * n * sizeof(double)));
         A->io_n = 6 * n;
     }
-    {
-        std::lock_guard<std::mutex> cg(ctx->mu);
-        if (!ctx->io_h2d) AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->io_h2d, cudaStreamNonBlocking));
-        if (!ctx->io_d2h) AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->io_d2h, cudaStreamNonBlocking));
-    }
+    if (!ctx->io_h2d) AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->io_h2d, cudaStreamNonBlocking));
+    if (!ctx->io_d2h) AMGP_CUDA(cudaStreamCreateWithFlags(&ctx->io_d2h, cudaStreamNonBlocking));
     const size_t bytes = (size_t)n * sizeof(double);
     double *db[2] = {A->io, A->io + 3 * n}, *dx0[2] = {A->io + n, A->io + 4 * n},
            *dx[2] = {A->io + 2 * n, A->io + 5 * n};
@@ -274,11 +273,35 @@ extern "C" int amgp_smoother_apply_host(amgp_ctx *ctx, amgp_mat *A, const double
     return st;
 }
 
+// out = a + s*b (sign > 0) or a - s*b (sign < 0): numpy's `a + s * b` with
+// the product rounded first (no FMA) -- the axpys of reference krylov.py:101-119.
+__global__ void k_vec_update(int64_t n, double s, const double *__restrict__ a, const double *__restrict__ b,
+                             double *__restrict__ out, int sign) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const double t = __dmul_rn(s, b[i]);
+        out[i] = sign > 0 ? __dadd_rn(a[i], t) : __dsub_rn(a[i], t);
+    }
+}
+
+extern "C" int amgp_vec_update(amgp_ctx *ctx, int64_t n, double s, const double *a, const double *b, double *out,
+                               int sign) {
+    if (!ctx || n < 0 || (n && (!a || !b || !out)) || sign == 0)
+        return amgp_fail(AMGP_EINVAL, "amgp_vec_update: bad argument");
+    if (n == 0) return AMGP_OK;
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> cg(ctx->mu);
+    const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, 256), 148 * 16);
+    k_vec_update<<<g, 256, 0, ctx->stream>>>(n, s, a, b, out, sign);
+    AMGP_CHECK_LAUNCH(ctx);
+    return AMGP_OK;
+}
+
 extern "C" int amgp_fused_update(amgp_ctx *ctx, int64_t n, double rho, double rho_prev, double c,
                                  const double *s, double *r, double *d, double *x) {
     if (!ctx || n < 0) return amgp_fail(AMGP_EINVAL, "fused_update: vector length mismatch");
     if (n == 0) return AMGP_OK;
     AMGP_CUDA(cudaSetDevice(ctx->device));
+    std::lock_guard<std::mutex> cg(ctx->mu);
     const double rp = rho * rho_prev;  // sparse.py:137 evaluates rho*rho_prev first
     const int blk = 256;
     const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, blk), 148 * 16);

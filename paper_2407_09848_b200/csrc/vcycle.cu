@@ -332,6 +332,7 @@ extern "C" int amgp_hier_set_smoother(amgp_hier *h, int level, const amgp_smooth
     if (!h) return amgp_fail(AMGP_EINVAL, "null hierarchy");
     SmootherPlan p;
     AMGP_TRY(make_smoother_plan(cfg, &p));
+    std::lock_guard<std::mutex> cg(h->ctx->mu);
     std::lock_guard<std::mutex> g(h->mu);
     if (level >= h->nlev) return amgp_fail(AMGP_EINVAL, "level out of range");
     for (int l = 0; l < h->nlev; l++)
@@ -349,6 +350,7 @@ extern "C" int amgp_hier_set_coarse_cholesky(amgp_hier *h, const double *L) {
     const int64_t n = h->A[h->nlev - 1]->nrows;
     if (n * (int64_t)sizeof(double) > 200 * 1024)
         return amgp_fail(AMGP_EINVAL, "coarse level too large for the dense device solve");
+    std::lock_guard<std::mutex> cg(h->ctx->mu);
     std::lock_guard<std::mutex> g(h->mu);
     cudaFree(h->cholL);
     h->cholL = nullptr;
@@ -364,6 +366,7 @@ extern "C" int amgp_hier_set_coarse_cholesky(amgp_hier *h, const double *L) {
 
 extern "C" int amgp_hier_use_graph(amgp_hier *h, int enable) {
     if (!h) return amgp_fail(AMGP_EINVAL, "null hierarchy");
+    std::lock_guard<std::mutex> cg(h->ctx->mu);
     std::lock_guard<std::mutex> g(h->mu);
     h->use_graph = enable != 0;
     return AMGP_OK;
@@ -389,6 +392,7 @@ extern "C" int amgp_vcycle_apply(amgp_hier *h, const double *r, double *z) {
     if (h->A[0]->nrows > 0 && (!r || !z)) return amgp_fail(AMGP_EINVAL, "null vector");
     if (r == z) return amgp_fail(AMGP_EINVAL, "r and z must not alias");
     AMGP_CUDA(cudaSetDevice(h->ctx->device));
+    std::lock_guard<std::mutex> cg(h->ctx->mu);
     std::lock_guard<std::mutex> g(h->mu);
     return vcycle_enqueue(h, r, z);
 }

@@ -121,7 +121,15 @@ class PolySmootherConfig:
 
 
 def _m_device(M, c):
-    return M.device(c)
+    """Device copy of an l1 diagonal: ours, or any object with an m_diag field
+    (the reference's L1JacobiData), uploaded once and cached on it."""
+    if hasattr(M, "device"):
+        return M.device(c)
+    d = getattr(M, "_b200_m", None)
+    if d is None:
+        d = N.to_device(M.m_diag, c)
+        M._b200_m = d
+    return d
 
 
 def smoother_apply(config, A, M, b, x0):

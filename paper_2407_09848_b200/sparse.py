@@ -251,13 +251,26 @@ class CsrMatrix:
         return d.nnz == 0 or np.max(np.abs(d.data)) <= rtol * scale
 
 
+def _csr_like(A):
+    return all(hasattr(A, k) for k in ("nrows", "ncols", "row_ptr", "col_idx", "values"))
+
+
 def device_of(A):
-    """DeviceMatrix of a CsrMatrix / DeviceMatrix; TypeError otherwise (the
-    dense spectral operators of the reference are out of scope)."""
+    """DeviceMatrix of a CsrMatrix / DeviceMatrix, or of any object with the
+    reference CsrMatrix fields (nrows, ncols, row_ptr, col_idx, values -- e.g.
+    the reference's own CsrMatrix, sparse.py:32-56), uploaded once and cached
+    on the object as the reference caches its scipy view (sparse.py:87-92).
+    TypeError otherwise (the dense spectral operators are out of scope)."""
     if isinstance(A, DeviceMatrix):
         return A
     if isinstance(A, CsrMatrix):
         return A.device()
+    if _csr_like(A):
+        D = getattr(A, "_b200_dev", None)
+        if D is None:
+            D = DeviceMatrix.from_csr(A)
+            A._b200_dev = D
+        return D
     raise TypeError(f"device operator must be CsrMatrix or DeviceMatrix, got {type(A).__name__}")
 
 

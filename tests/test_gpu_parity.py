@@ -528,3 +528,25 @@ def test_smoother_apply_batch_host_buffers_bitwise(P):
         assert np.array_equal(g.numpy(), P.smoother_apply(cfg, A, M, b, x0))
     with pytest.raises(ValueError):
         P.smoother_apply_batch(cfgs[:2], A, M, bs[:1], x0s[:2])
+
+
+@pytest.mark.parametrize("prefix", ["sa16", "mt8", "mt16"])
+def test_pcg_with_a_plain_callable_is_the_reference_bitwise(P, prefix):
+    """A preconditioner given as an arbitrary callable (the reference accepts
+    any r -> z, krylov.py:88) takes the reference-exact device path: OpenBLAS
+    order dots, numpy-rounded axpys -- iterations, the residual history and
+    the solution equal the reference's (goldens) bit for bit."""
+    d = golden("hier_small.npz")
+    fams = sorted({k.split("_pcg_")[1].rsplit("_k", 1)[0] for k in d if k.startswith(prefix + "_pcg_")})
+    for fam in fams:
+        for k in (1, 4):
+            key = f"{prefix}_pcg_{fam}_k{k}"
+            if key + "_iters" not in d:
+                continue
+            h, _ = golden_hierarchy(P, prefix, P.PolySmootherConfig(family=fam, degree=k))
+            n = h.levels[0].A.nrows
+            x, rep = P.solve(h.levels[0].A, np.ones(n), precond=lambda r: P.vcycle_apply(h, r),
+                             cfg=P.KrylovConfig(tol=1e-6, itmax=1000))
+            assert rep.iterations == int(d[key + "_iters"][0]), key
+            assert np.array_equal(np.array(rep.residual_history), d[key + "_hist"]), key
+            assert np.array_equal(x, d[key + "_x"]), key

@@ -421,11 +421,17 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, stron
     if comm is not None:
         dist.barrier()
     c = As[0].ctx
+    sampler = ClockSampler(torch.cuda.current_device())
+    sampler.start()
+    run()
+    torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.time()
     e0.record(c.stream)
     x, rep = run()
     e1.record(c.stream)
     torch.cuda.synchronize()
+    clocks = sampler.stop(wall0 - 0.5, time.time())
     t = torch.tensor([e0.elapsed_time(e1) / 1e3, rep.elapsed_s], device="cuda", dtype=torch.float64)
     if comm is not None:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -441,7 +447,8 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, stron
             "setup_s": setup_s, "iterations": rep.iterations, "final_relres": rep.final_relres,
             "solve_s": sec, "wall_s": float(t[1].item()), "tol": 1e-6, "krylov": variant,
             "replicate_below": replicate_below,
-            "roofline_rank0": solve_roofline(shapes, k, family, rep.iterations, sec, peak)}
+            "roofline_rank0": solve_roofline(shapes, k, family, rep.iterations, sec, peak),
+            "clocks_rank0": clocks}
 
 
 def run_b200(args):
@@ -638,6 +645,10 @@ def run_b200(args):
 
 
 def main():
+    if os.environ.get("AMGP_WATCHDOG"):  # diagnostics: Python stacks of a stuck run, then exit
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["AMGP_WATCHDOG"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)

@@ -87,14 +87,18 @@ struct amgp_ctx {
 // final ready/consumed signal, so reuse would need a collective in
 // amgp_mat_destroy (unsafe from garbage-collected owners).  4096 slots of
 // 16 words = 512 KB per context; ~3 slots per distributed level.
+#ifndef AMGP_MAX_SLOTS
 #define AMGP_MAX_SLOTS 4096
+#endif
 // per-slot synchronisation words of the p2p transport (u64, monotonic):
 //   [0, nranks)         ready[src]    -- epoch of the last halo src delivered here
 //   [nranks, 2 nranks)  consumed[dst] -- epoch whose halo dst has finished reading
 //   [2 nranks]          epoch         -- exchanges completed on this rank
 //   [2 nranks + 1]      ticket        -- pack-kernel CTAs done (last one signals)
 //   [2 nranks + 2]      ticket        -- boundary launch CTAs done (last one completes)
+#ifndef AMGP_SYNC_STRIDE
 #define AMGP_SYNC_STRIDE(nr) ((2 * (nr) + 3 + 15) / 16 * 16)
+#endif
 
 // Halo plan of a row-distributed matrix (dist.cu).  Columns [0, nown) are
 // the rank's own entries of the operand vector; columns >= nown index the
@@ -126,6 +130,19 @@ struct HaloPlan {
     unsigned long long **d_ready_remote = nullptr;     // [nsendp] ready[me] on each receiver
     unsigned long long **d_consumed_remote = nullptr;  // [nrecvp] consumed[me] on each sender
 };
+
+// The stream library work of a context is enqueued on.  A V-cycle graph is
+// captured on a private stream (vcycle.cu) named by this thread-local
+// override, so other host threads keep using ctx->stream meanwhile (their
+// launches can never end up inside the capture).
+struct CaptureOverride {
+    const amgp_ctx *ctx = nullptr;
+    cudaStream_t stream = nullptr;
+};
+extern thread_local CaptureOverride amgp_capture;
+inline cudaStream_t cur_stream(const amgp_ctx *ctx) {
+    return amgp_capture.ctx == ctx ? amgp_capture.stream : ctx->stream;
+}
 
 struct amgp_mat {
     amgp_ctx *ctx = nullptr;
@@ -284,7 +301,7 @@ int make_smoother_plan(const amgp_smoother_cfg *cfg, SmootherPlan *plan);
 // Workspace needed by smoother_enqueue for an n-row matrix (doubles).
 inline int64_t smoother_work_doubles(int64_t n) { return 4 * n; }
 
-// Enqueue one smoother application on ctx->stream.  x0 == nullptr: zero
+// Enqueue one smoother application on cur_stream(ctx).  x0 == nullptr: zero
 // initial guess.  x0 must not alias x.  work: smoother_work_doubles(n).
 int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const SmootherPlan &p,
                      const double *b, const double *x0, double *x, double *work);
@@ -332,13 +349,17 @@ __device__ __forceinline__ double ld_gather_f64(const double *p, uint64_t pol) {
     asm("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
     return v;
 }
-// Halo entries are written by a peer GPU while the kernel runs (p2p
-// transport): never through the non-coherent path, never hoisted above the
-// in-kernel halo wait (volatile, ordered after its acquire + barrier), and
-// cached at L2 only (the point of coherence for the peer's NVLink stores).
+// Gathers of a boundary launch (columns may index the halo, which a peer GPU
+// writes while the kernel runs on the p2p transport): never through the
+// non-coherent path, cached at L2 only (the point of coherence for the
+// peer's NVLink stores), and with a memory clobber so the compiler cannot
+// hoist them above the in-kernel halo wait (acquire + barrier).  One load
+// from a selected pointer per slot keeps the U gathers a single predicated
+// batch (a per-slot branch between two load kinds serialised them: 0.42 vs
+// 0.31 s per 635^3 solve on 4 GPUs).
 __device__ __forceinline__ double ld_halo_f64(const double *p) {
     double v;
-    asm volatile("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    asm("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
     return v;
 }
 
@@ -370,10 +391,10 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
 #pragma unroll
         for (int u = 0; u < U; u++) {
             if (HALO) {
-                // own entries through the read-only path, halo entries
-                // coherently (ld_halo_f64)
                 const int64_t c = cc[u];
-                xx[u] = c < 0 ? 0.0 : (c < A.nown ? ld_gather_f64(x + c, pl) : ld_halo_f64(xh + (c - A.nown)));
+                const bool own = c < A.nown;
+                const double *p = (own ? x : xh) + (own ? c : c - A.nown);
+                xx[u] = c < 0 ? 0.0 : ld_halo_f64(p);
             } else
                 xx[u] = cc[u] < 0 ? 0.0 : ld_gather_f64(x + cc[u], pl);
         }

@@ -4,6 +4,7 @@
 #include "amgp_common.cuh"
 
 static thread_local std::string g_last_error;
+thread_local CaptureOverride amgp_capture;
 
 void amgp_set_error(const std::string &msg) { g_last_error = msg; }
 

@@ -103,13 +103,13 @@ static int allgather_host(amgp_ctx *ctx, const void *mine, size_t bytes, std::ve
     AMGP_CUDA(cudaMalloc(&d, bytes * (ctx->nranks + 1)));
     AMGP_CUDA(cudaMemcpy(d + bytes * ctx->nranks, mine, bytes, cudaMemcpyHostToDevice));
     ncclResult_t r = api->AllGather(d + bytes * ctx->nranks, d, bytes, ncclChar,
-                                    (ncclComm_t)ctx->comm, ctx->stream);
+                                    (ncclComm_t)ctx->comm, cur_stream(ctx));
     if (r != ncclSuccess) {
         cudaFree(d);
         return amgp_fail(AMGP_ENCCL, "allgather failed");
     }
     all.resize(bytes * ctx->nranks);
-    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    AMGP_CUDA(cudaStreamSynchronize(cur_stream(ctx)));
     AMGP_CUDA(cudaMemcpy(all.data(), d, all.size(), cudaMemcpyDeviceToHost));
     cudaFree(d);
     return AMGP_OK;
@@ -480,7 +480,7 @@ __global__ void k_halo_signal(unsigned long long *sync, int nranks, int nrecvp,
 static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
     if (h.nsend == 0) return AMGP_OK;
     cudaStream_t st = ctx->comm_stream;
-    AMGP_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
+    AMGP_CUDA(cudaEventRecord(ctx->ev_packed, cur_stream(ctx)));
     AMGP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
     // launched with the highest priority explicitly (kept when captured into
     // a graph): its CTAs must be scheduled ahead of the interior rows
@@ -505,7 +505,7 @@ static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
 static int p2p_end(amgp_ctx *ctx, const HaloPlan &h) {
     // the pack kernel must not be overtaken by the next exchange's; the
     // data itself is awaited inside the boundary kernels (halo_wait)
-    if (h.nsend > 0) AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
+    if (h.nsend > 0) AMGP_CUDA(cudaStreamWaitEvent(cur_stream(ctx), ctx->ev_exchanged, 0));
     return AMGP_OK;
 }
 
@@ -513,7 +513,7 @@ int halo_exchange_done(amgp_ctx *ctx, const amgp_mat *A) {
     if (!ctx->halo_p2p) return AMGP_OK;
     const HaloPlan &h = *A->halo;
     if (h.peers.empty()) return AMGP_OK;
-    k_halo_signal<<<1, 32, 0, ctx->stream>>>(h.sync_slot, ctx->nranks, h.nrecvp, h.d_consumed_remote);
+    k_halo_signal<<<1, 32, 0, cur_stream(ctx)>>>(h.sync_slot, ctx->nranks, h.nrecvp, h.d_consumed_remote);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }
@@ -525,10 +525,10 @@ int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
     if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator for the halo exchange");
     if (h.nsend > 0) {
         const unsigned g = (unsigned)std::min<int64_t>(grid_for(h.nsend, 256), 148 * 8);
-        k_pack<<<g, 256, 0, ctx->stream>>>(h.nsend, h.send_idx, x, h.sendbuf);
+        k_pack<<<g, 256, 0, cur_stream(ctx)>>>(h.nsend, h.send_idx, x, h.sendbuf);
         AMGP_CHECK_LAUNCH(ctx);
     }
-    AMGP_CUDA(cudaEventRecord(ctx->ev_packed, ctx->stream));
+    AMGP_CUDA(cudaEventRecord(ctx->ev_packed, cur_stream(ctx)));
     AMGP_CUDA(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_packed, 0));
     ncclComm_t comm = (ncclComm_t)ctx->comm;
     NCCL_TRY(api->GroupStart());
@@ -547,7 +547,7 @@ int halo_exchange_begin(amgp_ctx *ctx, const amgp_mat *A, const double *x) {
 
 int halo_exchange_end(amgp_ctx *ctx, const amgp_mat *A) {
     if (ctx->halo_p2p) return p2p_end(ctx, *A->halo);
-    AMGP_CUDA(cudaStreamWaitEvent(ctx->stream, ctx->ev_exchanged, 0));
+    AMGP_CUDA(cudaStreamWaitEvent(cur_stream(ctx), ctx->ev_exchanged, 0));
     return AMGP_OK;
 }
 
@@ -566,8 +566,8 @@ int allreduce_sum_ordered(amgp_ctx *ctx, const double *local, int nv, double *ou
     if (!api || !ctx->comm) return amgp_fail(AMGP_ENCCL, "no communicator");
     if (nv > 16) return amgp_fail(AMGP_EINVAL, "too many reduction values");
     NCCL_TRY(api->AllGather(local, ctx->gather_buf, (size_t)nv, ncclDouble, (ncclComm_t)ctx->comm,
-                            ctx->stream));
-    k_fold_ranks<<<1, 32, 0, ctx->stream>>>(ctx->gather_buf, ctx->nranks, nv, out);
+                            cur_stream(ctx)));
+    k_fold_ranks<<<1, 32, 0, cur_stream(ctx)>>>(ctx->gather_buf, ctx->nranks, nv, out);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }
@@ -617,14 +617,14 @@ int refresh_slice_maxcol(amgp_mat *A) {
     int *bad = nullptr;
     AMGP_CUDA(cudaMalloc(&d, A->nslices * sizeof(int64_t)));
     AMGP_CUDA(cudaMalloc(&bad, sizeof(int)));
-    AMGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
-    k_slice_maxcol<<<grid_for(A->nslices * 32, 256), 256, 0, ctx->stream>>>(view_of(A), d, bad);
+    AMGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), cur_stream(ctx)));
+    k_slice_maxcol<<<grid_for(A->nslices * 32, 256), 256, 0, cur_stream(ctx)>>>(view_of(A), d, bad);
     AMGP_CHECK_LAUNCH(ctx);
     int hbad = 0;
     AMGP_CUDA(cudaMemcpyAsync(A->slice_maxcol.data(), d, A->nslices * sizeof(int64_t),
-                              cudaMemcpyDeviceToHost, ctx->stream));
-    AMGP_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+                              cudaMemcpyDeviceToHost, cur_stream(ctx)));
+    AMGP_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, cur_stream(ctx)));
+    AMGP_CUDA(cudaStreamSynchronize(cur_stream(ctx)));
     cudaFree(d);
     cudaFree(bad);
     if (hbad) return amgp_fail(AMGP_EINVAL, "column outside the owned range and every halo segment");
@@ -649,10 +649,10 @@ extern "C" int amgp_mat_localize(amgp_mat *A, int64_t own_lo, int64_t own_hi, in
     AMGP_CUDA(cudaMemcpy(dseg, seg.data(), seg.size() * sizeof(int64_t), cudaMemcpyHostToDevice));
     if (A->stored > 0) {
         const unsigned g = (unsigned)std::min<int64_t>(grid_for(A->stored, 256), 148 * 16);
-        k_localize<<<g, 256, 0, ctx->stream>>>(A->stored, A->col, own_lo, own_hi, nseg, dseg);
+        k_localize<<<g, 256, 0, cur_stream(ctx)>>>(A->stored, A->col, own_lo, own_hi, nseg, dseg);
         AMGP_CHECK_LAUNCH(ctx);
     }
-    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    AMGP_CUDA(cudaStreamSynchronize(cur_stream(ctx)));
     cudaFree(dseg);
     A->ncols = (own_hi - own_lo) + base;
     A->row_offset = 0;  // rows now index the local block; diagonal at column = row

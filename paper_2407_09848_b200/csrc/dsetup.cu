@@ -668,7 +668,7 @@ int amgp_ds_diag(amgp_mat *A, double *d) {
     amgp_ctx *ctx = A->ctx;
     AMGP_CUDA(cudaSetDevice(ctx->device));
     if (A->nrows == 0) return AMGP_OK;
-    k_ds_diag<<<grid_for(A->nrows, 256), 256, 0, ctx->stream>>>(view_of(A), d);
+    k_ds_diag<<<grid_for(A->nrows, 256), 256, 0, cur_stream(ctx)>>>(view_of(A), d);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }
@@ -680,7 +680,7 @@ int amgp_ds_strength(amgp_mat *A, const double *d, double theta, int64_t nown, c
     amgp_ctx *ctx = A->ctx;
     AMGP_CUDA(cudaSetDevice(ctx->device));
     if (nlist == 0) return AMGP_OK;
-    k_ds_strength<<<grid_for(nlist, 256), 256, 0, ctx->stream>>>(view_of(A), d, theta, nown, rows, nlist, off,
+    k_ds_strength<<<grid_for(nlist, 256), 256, 0, cur_stream(ctx)>>>(view_of(A), d, theta, nown, rows, nlist, off,
                                                                  cnt, scol, sabs);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
@@ -708,13 +708,13 @@ static int blas_dot3_enqueue(amgp_ctx *ctx, int64_t n, const double *x, const do
     for (const auto &c : ch)
         aligned &= ((reinterpret_cast<uintptr_t>(x + c.start) | reinterpret_cast<uintptr_t>(y + c.start)) & 15) == 0;
     AMGP_CUDA(cudaMemcpyAsync(dchunks, ch.data(), ch.size() * sizeof(DotChunk), cudaMemcpyHostToDevice,
-                              ctx->stream));
+                              cur_stream(ctx)));
     const size_t smem = aligned ? (size_t)2 * DOT_STAGES * DOT_CH * sizeof(double) : 0;
     AMGP_CUDA(cudaFuncSetAttribute(k_blas_dot3, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    2 * DOT_STAGES * DOT_CH * (int)sizeof(double)));
-    k_blas_dot3<<<(unsigned)ch.size(), 64, smem, ctx->stream>>>(x, y, dchunks, aligned ? 1 : 0, part);
+    k_blas_dot3<<<(unsigned)ch.size(), 64, smem, cur_stream(ctx)>>>(x, y, dchunks, aligned ? 1 : 0, part);
     AMGP_CHECK_LAUNCH(ctx);
-    k_blas_fold<<<1, 32, 0, ctx->stream>>>(part, (int)ch.size(), out);
+    k_blas_fold<<<1, 32, 0, cur_stream(ctx)>>>(part, (int)ch.size(), out);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }
@@ -734,8 +734,8 @@ int amgp_ds_blas_dot3(amgp_ctx *ctx, int64_t n, const double *x, const double *y
     int st = blas_dot3_enqueue(ctx, n, x, y, std::min(threads, 64), buf, dch, buf + 3 * 64);
     if (st == AMGP_OK) {
         cudaError_t e = cudaMemcpyAsync(out_host, buf + 3 * 64, 3 * sizeof(double), cudaMemcpyDeviceToHost,
-                                        ctx->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+                                        cur_stream(ctx));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
         if (e != cudaSuccess) st = amgp_cuda_fail(e, "blas_dot3", __FILE__, __LINE__);
     }
     cudaFree(buf);
@@ -761,45 +761,45 @@ int amgp_ds_lambda_max(amgp_ctx *ctx, amgp_mat *A, const double *d, double *v, i
     double *part = buf + 4 * nb, *sc = part + 3 * 64;  // sc: lam, nrm, stop, -, dots[3] at 4, folded at 8
     int st = AMGP_OK;
     auto run = [&]() -> int {
-        AMGP_CUDA(cudaMemsetAsync(sc, 0, 16 * sizeof(double), ctx->stream));
+        AMGP_CUDA(cudaMemsetAsync(sc, 0, 16 * sizeof(double), cur_stream(ctx)));
         const int g = launch_grid(n, 256);
         if (n) {
-            k_ds_sqrt<<<g, 256, 0, ctx->stream>>>(n, d, ds);
+            k_ds_sqrt<<<g, 256, 0, cur_stream(ctx)>>>(n, d, ds);
             AMGP_CHECK_LAUNCH(ctx);
         }
         for (int it = 0; it < iters; it++) {
             if (n) {
-                k_ds_div<<<g, 256, 0, ctx->stream>>>(n, v, ds, u);
+                k_ds_div<<<g, 256, 0, cur_stream(ctx)>>>(n, v, ds, u);
                 AMGP_CHECK_LAUNCH(ctx);
             }
             AMGP_TRY(spmv_enqueue(ctx, A, u, y));
             if (n) {
-                k_ds_div<<<g, 256, 0, ctx->stream>>>(n, y, ds, w);
+                k_ds_div<<<g, 256, 0, cur_stream(ctx)>>>(n, y, ds, w);
                 AMGP_CHECK_LAUNCH(ctx);
                 AMGP_TRY(blas_dot3_enqueue(ctx, n, v, w, std::min(threads, 64), part, dch, sc + 4));
             } else {
-                AMGP_CUDA(cudaMemsetAsync(sc + 4, 0, 3 * sizeof(double), ctx->stream));
+                AMGP_CUDA(cudaMemsetAsync(sc + 4, 0, 3 * sizeof(double), cur_stream(ctx)));
             }
             const double *tot = sc + 4;
             if (fold_ranks && ctx->nranks > 1) {
                 AMGP_TRY(allreduce_sum_ordered(ctx, sc + 4, 3, sc + 8));
                 tot = sc + 8;
             }
-            k_power_scalars<<<1, 32, 0, ctx->stream>>>(tot, sc);
+            k_power_scalars<<<1, 32, 0, cur_stream(ctx)>>>(tot, sc);
             AMGP_CHECK_LAUNCH(ctx);
             if (n) {
-                k_ds_scale<<<g, 256, 0, ctx->stream>>>(n, w, sc, v);
+                k_ds_scale<<<g, 256, 0, cur_stream(ctx)>>>(n, w, sc, v);
                 AMGP_CHECK_LAUNCH(ctx);
             }
         }
         double h[3] = {1.0, 0.0, 0.0};
-        AMGP_CUDA(cudaMemcpyAsync(h, sc, 3 * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream));
-        AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+        AMGP_CUDA(cudaMemcpyAsync(h, sc, 3 * sizeof(double), cudaMemcpyDeviceToHost, cur_stream(ctx)));
+        AMGP_CUDA(cudaStreamSynchronize(cur_stream(ctx)));
         *lam = iters == 0 ? 1.0 : (h[2] != 0.0 ? 0.0 : h[0]);
         return AMGP_OK;
     };
     st = run();
-    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(cur_stream(ctx));
     cudaFree(buf);
     cudaFree(dch);
     return st;
@@ -828,10 +828,10 @@ int amgp_ds_prolongator(amgp_mat *A, const double *d, const int64_t *agg_own, co
     double *sv = nullptr;
     AMGP_CUDA(cudaMalloc(&sk, (size_t)nthr * cap * sizeof(int64_t)));
     AMGP_CUDA(cudaMalloc(&sv, (size_t)nthr * cap * sizeof(double)));
-    k_ds_prolong<<<grid, block, 0, ctx->stream>>>(view_of(A), d, agg_own, agg_halo, nown, omega, smooth, row_ptr,
+    k_ds_prolong<<<grid, block, 0, cur_stream(ctx)>>>(view_of(A), d, agg_own, agg_halo, nown, omega, smooth, row_ptr,
                                                   row_cnt, col, val, sk, sv, cap);
     cudaError_t e = cudaGetLastError();
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
     cudaFree(sk);
     cudaFree(sv);
     if (e != cudaSuccess) return amgp_cuda_fail(e, "k_ds_prolong", __FILE__, __LINE__);
@@ -877,15 +877,15 @@ int amgp_ds_spgemm(amgp_ctx *ctx, const amgp_mat *A_sell, const int64_t *a_rp, c
         return st;
     };
     do {
-        cudaError_t e = cudaMemsetAsync(novf, 0, 2 * sizeof(unsigned long long), ctx->stream);
+        cudaError_t e = cudaMemsetAsync(novf, 0, 2 * sizeof(unsigned long long), cur_stream(ctx));
         if (e != cudaSuccess) { fail(e, "memset"); break; }
         // stage 1: 128-slot shared tables, 8 warps per CTA
-        k_ds_spgemm<8, 128, false><<<launch_grid(nrows, 8, 148 * 32), 256, spgemm_smem(8, 128), ctx->stream>>>(
+        k_ds_spgemm<8, 128, false><<<launch_grid(nrows, 8, 148 * 32), 256, spgemm_smem(8, 128), cur_stream(ctx)>>>(
             a, b, a_rows, nullptr, nrows, row_ptr, row_cnt, c_col, c_val, ovf, novf, nullptr, nullptr, nullptr);
         if ((e = cudaGetLastError()) != cudaSuccess) { fail(e, "k_ds_spgemm<128>"); break; }
         unsigned long long h[2] = {0, 0};
-        e = cudaMemcpyAsync(h, novf, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        e = cudaMemcpyAsync(h, novf, sizeof(h), cudaMemcpyDeviceToHost, cur_stream(ctx));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
         if (e != cudaSuccess) { fail(e, "spgemm overflow count"); break; }
         if (h[0] == 0) break;
         // stage 2: 1024-slot shared tables (4 warps x 20 KB)
@@ -893,11 +893,11 @@ int amgp_ds_spgemm(amgp_ctx *ctx, const amgp_mat *A_sell, const int64_t *a_rp, c
                                  (int)spgemm_smem(4, 1024));
         if (e != cudaSuccess) { fail(e, "spgemm smem attribute"); break; }
         k_ds_spgemm<4, 1024, false><<<launch_grid((int64_t)h[0], 4, 148 * 8), 128, spgemm_smem(4, 1024),
-                                      ctx->stream>>>(a, b, a_rows, ovf, (int64_t)h[0], row_ptr, row_cnt, c_col,
+                                      cur_stream(ctx)>>>(a, b, a_rows, ovf, (int64_t)h[0], row_ptr, row_cnt, c_col,
                                                      c_val, ovf + nrows, novf + 1, nullptr, nullptr, nullptr);
         if ((e = cudaGetLastError()) != cudaSuccess) { fail(e, "k_ds_spgemm<1024>"); break; }
-        e = cudaMemcpyAsync(h, novf, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        e = cudaMemcpyAsync(h, novf, sizeof(h), cudaMemcpyDeviceToHost, cur_stream(ctx));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
         if (e != cudaSuccess) { fail(e, "spgemm overflow count"); break; }
         if (h[1] == 0) break;
         // stage 3: 65536-slot per-warp tables in global memory
@@ -906,16 +906,16 @@ int amgp_ds_spgemm(amgp_ctx *ctx, const amgp_mat *A_sell, const int64_t *a_rp, c
         if ((e = cudaMalloc(&gk, (size_t)nw * HG * sizeof(int64_t))) != cudaSuccess) { fail(e, "alloc"); break; }
         if ((e = cudaMalloc(&gv, (size_t)nw * HG * sizeof(double))) != cudaSuccess) { fail(e, "alloc"); break; }
         if ((e = cudaMalloc(&gs, (size_t)nw * HG * sizeof(int32_t))) != cudaSuccess) { fail(e, "alloc"); break; }
-        e = cudaMemsetAsync(novf, 0, sizeof(unsigned long long), ctx->stream);
-        k_ds_spgemm<1, HG, true><<<nw, 32, 0, ctx->stream>>>(a, b, a_rows, ovf + nrows, (int64_t)h[1], row_ptr,
+        e = cudaMemsetAsync(novf, 0, sizeof(unsigned long long), cur_stream(ctx));
+        k_ds_spgemm<1, HG, true><<<nw, 32, 0, cur_stream(ctx)>>>(a, b, a_rows, ovf + nrows, (int64_t)h[1], row_ptr,
                                                               row_cnt, c_col, c_val, ovf, novf, gk, gv, gs);
         if ((e = cudaGetLastError()) != cudaSuccess) { fail(e, "k_ds_spgemm<global>"); break; }
-        e = cudaMemcpyAsync(h, novf, sizeof(unsigned long long), cudaMemcpyDeviceToHost, ctx->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        e = cudaMemcpyAsync(h, novf, sizeof(unsigned long long), cudaMemcpyDeviceToHost, cur_stream(ctx));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
         if (e != cudaSuccess) { fail(e, "spgemm overflow count"); break; }
         if (h[0] != 0) st = amgp_fail(AMGP_EINVAL, "spgemm: output row exceeds 65472 entries");
     } while (false);
-    cudaStreamSynchronize(ctx->stream);
+    cudaStreamSynchronize(cur_stream(ctx));
     cudaFree(ovf);
     cudaFree(novf);
     cudaFree(gk);
@@ -932,7 +932,7 @@ int amgp_ds_symmetrize(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, const int6
         return amgp_fail(AMGP_EINVAL, "amgp_ds_symmetrize: bad argument");
     AMGP_CUDA(cudaSetDevice(ctx->device));
     if (n == 0) return AMGP_OK;
-    k_ds_symmetrize<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, g_rp, g_col, g_val, t_rp, t_col, t_val, row_ptr,
+    k_ds_symmetrize<<<grid_for(n, 256), 256, 0, cur_stream(ctx)>>>(n, g_rp, g_col, g_val, t_rp, t_col, t_val, row_ptr,
                                                                row_cnt, col, val);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
@@ -950,15 +950,15 @@ int amgp_ds_sym_lookup(amgp_ctx *ctx, int64_t n, const int64_t *rp, const int64_
     if (n == 0) return AMGP_OK;
     unsigned long long *d = nullptr;
     AMGP_CUDA(cudaMalloc(&d, sizeof(unsigned long long)));
-    cudaError_t e = cudaMemsetAsync(d, 0, sizeof(unsigned long long), ctx->stream);
+    cudaError_t e = cudaMemsetAsync(d, 0, sizeof(unsigned long long), cur_stream(ctx));
     if (e == cudaSuccess) {
-        k_ds_sym_lookup<<<grid_for(n * 32, 256), 256, 0, ctx->stream>>>(n, rp, col, val, gt, orow, ocol, oval, d,
+        k_ds_sym_lookup<<<grid_for(n * 32, 256), 256, 0, cur_stream(ctx)>>>(n, rp, col, val, gt, orow, ocol, oval, d,
                                                                       (unsigned long long)cap);
         e = cudaGetLastError();
     }
     unsigned long long h = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, cur_stream(ctx));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
     cudaFree(d);
     if (e != cudaSuccess) return amgp_cuda_fail(e, "k_ds_sym_lookup", __FILE__, __LINE__);
     ctx->launches.fetch_add(1);
@@ -974,7 +974,7 @@ int amgp_ds_symmetrize_lookup(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, con
         return amgp_fail(AMGP_EINVAL, "amgp_ds_symmetrize_lookup: bad argument");
     AMGP_CUDA(cudaSetDevice(ctx->device));
     if (n == 0) return AMGP_OK;
-    k_ds_symmetrize_lookup<<<grid_for(n, 256), 256, 0, ctx->stream>>>(n, g_rp, g_col, g_val, gt, o_rp, o_col, o_val,
+    k_ds_symmetrize_lookup<<<grid_for(n, 256), 256, 0, cur_stream(ctx)>>>(n, g_rp, g_col, g_val, gt, o_rp, o_col, o_val,
                                                                       row_ptr, row_cnt, col, val);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
@@ -991,19 +991,19 @@ int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_
     AMGP_CUDA(cudaSetDevice(ctx->device));
     const int64_t ns = (nrows + 31) / 32;
     int64_t nnz = 0;
-    if (nrows) AMGP_CUDA(cudaMemcpyAsync(&nnz, rp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, ctx->stream));
+    if (nrows) AMGP_CUDA(cudaMemcpyAsync(&nnz, rp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, cur_stream(ctx)));
     std::vector<int32_t> w(std::max<int64_t>(ns, 1));
     if (ns) {
         int32_t *dw = nullptr;
         AMGP_CUDA(cudaMalloc(&dw, ns * sizeof(int32_t)));
-        k_dcsr_width<<<grid_for(ns * 32, 256), 256, 0, ctx->stream>>>(nrows, rp, dw);
+        k_dcsr_width<<<grid_for(ns * 32, 256), 256, 0, cur_stream(ctx)>>>(nrows, rp, dw);
         cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaMemcpyAsync(w.data(), dw, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream);
-        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(w.data(), dw, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, cur_stream(ctx));
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
         cudaFree(dw);
         if (e != cudaSuccess) return amgp_cuda_fail(e, "k_dcsr_width", __FILE__, __LINE__);
     } else {
-        AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+        AMGP_CUDA(cudaStreamSynchronize(cur_stream(ctx)));
     }
     std::vector<int64_t> sp(ns + 1);
     int64_t stored = 0;
@@ -1019,17 +1019,17 @@ int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_
     A->max_width = wmax;
     int *bad = nullptr;
     cudaError_t e = cudaMemcpyAsync(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
-                                    ctx->stream);
+                                    cur_stream(ctx));
     if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(int));
-    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), cur_stream(ctx));
     if (e == cudaSuccess && ns) {
-        k_dcsr_fill<<<grid_for(ns * 32, 256), 256, 0, ctx->stream>>>(nrows, ncols, rp, col, val, A->slice_ptr,
+        k_dcsr_fill<<<grid_for(ns * 32, 256), 256, 0, cur_stream(ctx)>>>(nrows, ncols, rp, col, val, A->slice_ptr,
                                                                      A->col, A->val, bad);
         e = cudaGetLastError();
     }
     int hbad = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, cur_stream(ctx));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
     cudaFree(bad);
     if (e != cudaSuccess) {
         amgp_mat_destroy(A);

@@ -126,7 +126,7 @@ extern "C" int amgp_mat_destroy(amgp_mat *A) {
     if (!A) return AMGP_OK;
     if (A->ctx) {
         cudaSetDevice(A->ctx->device);
-        cudaStreamSynchronize(A->ctx->stream);
+        cudaStreamSynchronize(cur_stream(A->ctx));
         if (A->ctx->comm_stream) cudaStreamSynchronize(A->ctx->comm_stream);  // halo pack kernels
     }
     mat_free_halo(A);
@@ -155,7 +155,7 @@ extern "C" int amgp_mat_to_csr(amgp_mat *A, int64_t *row_ptr, int64_t *col_idx, 
     std::vector<int64_t> sp(A->nslices + 1);
     std::vector<int32_t> col(std::max<int64_t>(A->stored, 1));
     std::vector<double> val(std::max<int64_t>(A->stored, 1));
-    AMGP_CUDA(cudaStreamSynchronize(A->ctx->stream));
+    AMGP_CUDA(cudaStreamSynchronize(cur_stream(A->ctx)));
     AMGP_CUDA(cudaMemcpy(sp.data(), A->slice_ptr, sp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
     if (A->stored > 0) {
         AMGP_CUDA(cudaMemcpy(col.data(), A->col, A->stored * sizeof(int32_t), cudaMemcpyDeviceToHost));
@@ -263,14 +263,14 @@ extern "C" int amgp_mat_poisson3d(amgp_ctx *ctx, int64_t m, int stencil, int64_t
     AMGP_CUDA(cudaMalloc(&dw, std::max<int64_t>(ns, 1) * sizeof(int32_t)));
     const int blk = 256;
     if (ns > 0) {
-        k_poisson_widths<<<grid_for(ns * 32, blk), blk, 0, ctx->stream>>>(m, stencil, row_begin, nrows, dw);
+        k_poisson_widths<<<grid_for(ns * 32, blk), blk, 0, cur_stream(ctx)>>>(m, stencil, row_begin, nrows, dw);
         cudaError_t e = cudaGetLastError();
         if (e != cudaSuccess) { cudaFree(dw); return amgp_cuda_fail(e, "k_poisson_widths", __FILE__, __LINE__); }
     }
     std::vector<int32_t> w(std::max<int64_t>(ns, 1));
     std::vector<int64_t> sp(ns + 1);
-    cudaError_t e = cudaMemcpyAsync(w.data(), dw, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, ctx->stream);
-    if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+    cudaError_t e = cudaMemcpyAsync(w.data(), dw, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, cur_stream(ctx));
+    if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
     cudaFree(dw);
     if (e != cudaSuccess) return amgp_cuda_fail(e, "poisson widths", __FILE__, __LINE__);
     int64_t stored = 0;
@@ -285,13 +285,13 @@ extern "C" int amgp_mat_poisson3d(amgp_ctx *ctx, int64_t m, int stencil, int64_t
     AMGP_TRY(mat_alloc(ctx, nrows, n, 0, ns, stored, &A));
     A->max_width = wmax;
     A->row_offset = row_begin;
-    e = cudaMemcpyAsync(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, ctx->stream);
+    e = cudaMemcpyAsync(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, cur_stream(ctx));
     if (e != cudaSuccess) { amgp_mat_destroy(A); return amgp_cuda_fail(e, "slice_ptr upload", __FILE__, __LINE__); }
     if (ns > 0) {
-        k_poisson_fill<<<grid_for(ns * 32, blk), blk, 0, ctx->stream>>>(m, stencil, row_begin, nrows,
+        k_poisson_fill<<<grid_for(ns * 32, blk), blk, 0, cur_stream(ctx)>>>(m, stencil, row_begin, nrows,
                                                                        A->slice_ptr, A->col, A->val);
         e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaStreamSynchronize(ctx->stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
         if (e != cudaSuccess) { amgp_mat_destroy(A); return amgp_cuda_fail(e, "k_poisson_fill", __FILE__, __LINE__); }
         ctx->launches.fetch_add(2);
     }
@@ -378,17 +378,17 @@ extern "C" int amgp_mat_l1_diag(amgp_mat *A, double *m_dev) {
     if (A->row_offset + A->nrows > A->ncols) return amgp_fail(AMGP_EINVAL, "matrix must be square");
     int *bad = nullptr;
     AMGP_CUDA(cudaMalloc(&bad, sizeof(int)));
-    AMGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), ctx->stream));
+    AMGP_CUDA(cudaMemsetAsync(bad, 0, sizeof(int), cur_stream(ctx)));
     // Generated row blocks store global columns: local row i is global row
     // row_offset + i.
     const int64_t off = A->row_offset;
     if (A->nslices > 0) {
-        k_l1_diag<<<grid_for(A->nslices * 32, 256), 256, 0, ctx->stream>>>(view_of(A), off, m_dev, bad);
+        k_l1_diag<<<grid_for(A->nslices * 32, 256), 256, 0, cur_stream(ctx)>>>(view_of(A), off, m_dev, bad);
         AMGP_CHECK_LAUNCH(ctx);
     }
     int hbad = 0;
-    AMGP_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, ctx->stream));
-    AMGP_CUDA(cudaStreamSynchronize(ctx->stream));
+    AMGP_CUDA(cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, cur_stream(ctx)));
+    AMGP_CUDA(cudaStreamSynchronize(cur_stream(ctx)));
     cudaFree(bad);
     if (hbad) return amgp_fail(AMGP_EINVAL, "non-positive diagonal entry");
     return AMGP_OK;

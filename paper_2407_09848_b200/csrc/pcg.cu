@@ -255,13 +255,13 @@ struct PcgWork {  // views into the context's cached PCG workspace
 int pcg_workspace(amgp_ctx *ctx, int64_t n, PcgWork *w) {
     const int64_t need = 5 * std::max<int64_t>(n, 1) + 3 * RGRID_MAX + 8;
     if (ctx->red_partial_n < need) {
-        cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(cur_stream(ctx));
         cudaFree(ctx->red_partial);
         ctx->red_partial = nullptr;
         ctx->red_partial_n = 0;
         AMGP_CUDA(cudaMalloc(&ctx->red_partial, need * sizeof(double)));
         ctx->red_partial_n = need;
-        AMGP_CUDA(cudaMemsetAsync(ctx->red_partial, 0, need * sizeof(double), ctx->stream));
+        AMGP_CUDA(cudaMemsetAsync(ctx->red_partial, 0, need * sizeof(double), cur_stream(ctx)));
     }
     double *p = ctx->red_partial;
     const int64_t nn = std::max<int64_t>(n, 1);
@@ -302,7 +302,7 @@ extern "C" int amgp_pcg_solve(amgp_ctx *ctx, amgp_mat *A, amgp_hier *h, const do
     // row-distributed solve: the fine matrix carries a halo plan (a single-GPU
     // solve on a multi-rank context stays local)
     const bool dist = ctx->comm != nullptr && ctx->nranks > 1 && A->halo != nullptr;
-    cudaStream_t st = ctx->stream;
+    cudaStream_t st = cur_stream(ctx);
     double *sc = ctx->scalars, *hs = ctx->host_scalars;
 
     PcgWork w;

@@ -109,9 +109,9 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                     // own entries through the read-only path, halo entries coherently
                     const int64_t c = cc[u];
                     if (c >= 0) {
-                        const double xv = halo && c >= A.nown ? ld_halo_f64(xh + (c - A.nown))
-                                                              : ld_gather_f64(xg + c, pl);
-                        p = __dmul_rn(vv[u], xv);
+                        const bool hc = halo && c >= A.nown;
+                        const double *src = (hc ? xh : xg) + (hc ? c - A.nown : c);
+                        p = __dmul_rn(vv[u], halo ? ld_halo_f64(src) : ld_gather_f64(src, pl));
                     }
                     prod[jj * 32 + lane] = p;
                 }
@@ -160,9 +160,10 @@ __device__ __forceinline__ double sell_row_dot_deep(const SellView &A, int64_t s
 #pragma unroll
         for (int u = 0; u < U; u++) {
             const int64_t cu = cc[u];
-            if (HALO)
-                xx[u] = cu < 0 ? 0.0 : (cu < A.nown ? ld_gather_f64(x + cu, pl) : ld_halo_f64(xh + (cu - A.nown)));
-            else
+            if (HALO) {
+                const bool own = cu < A.nown;
+                xx[u] = cu < 0 ? 0.0 : ld_halo_f64((own ? x : xh) + (own ? cu : cu - A.nown));
+            } else
                 xx[u] = cu < 0 ? 0.0 : ld_gather_f64(x + cu, pl);
         }
         int32_t nc[U];
@@ -228,9 +229,9 @@ void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const dou
     const int rv = rows_variant();
     if (split && v.nlist >= 2 * 148 && rv >= 8) {  // deep thread-per-row (experiment)
         const unsigned g = grid_for(v.nlist, DEEP_WARPS);
-        if (rv == 8) k_deep_rows<Epi, MODE, 8><<<g, DEEP_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
-        else if (rv == 16) k_deep_rows<Epi, MODE, 16><<<g, DEEP_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
-        else k_deep_rows<Epi, MODE, 24><<<g, DEEP_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+        if (rv == 8) k_deep_rows<Epi, MODE, 8><<<g, DEEP_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
+        else if (rv == 16) k_deep_rows<Epi, MODE, 16><<<g, DEEP_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
+        else k_deep_rows<Epi, MODE, 24><<<g, DEEP_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
         return;
     }
     const int nw = v.nlist < 2 * 148 ? 24 : SPLIT_WARPS;
@@ -238,11 +239,11 @@ void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const dou
     const unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);
     if (split) {
         if (nw == 24)
-            k_split_rows<Epi, MODE, 24, 8><<<grid, 24 * 32, 0, ctx->stream>>>(v, xg, epi);
+            k_split_rows<Epi, MODE, 24, 8><<<grid, 24 * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
         else
-            k_split_rows<Epi, MODE, SPLIT_WARPS, SPLIT_U><<<grid, SPLIT_WARPS * 32, 0, ctx->stream>>>(v, xg, epi);
+            k_split_rows<Epi, MODE, SPLIT_WARPS, SPLIT_U><<<grid, SPLIT_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
     } else {
-        k_thread_rows<Epi, MODE><<<grid, ROWS_BLOCK, 0, ctx->stream>>>(v, xg, epi);
+        k_thread_rows<Epi, MODE><<<grid, ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, xg, epi);
     }
 }
 

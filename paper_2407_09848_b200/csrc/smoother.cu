@@ -167,7 +167,7 @@ int smoother_enqueue(amgp_ctx *ctx, const amgp_mat *A, const double *m, const Sm
 
 static int ensure_work(amgp_mat *A, int64_t doubles) {
     if (A->work_n >= doubles) return AMGP_OK;
-    cudaStreamSynchronize(A->ctx->stream);
+    cudaStreamSynchronize(cur_stream(A->ctx));
     cudaFree(A->work);
     A->work = nullptr;
     A->work_n = 0;
@@ -192,7 +192,7 @@ extern "C" int amgp_smoother_apply(amgp_ctx *ctx, amgp_mat *A, const double *m,
     AMGP_TRY(ensure_work(A, smoother_work_doubles(n) + n));
     if (x0 && x0 == x) {  // x0 may alias x: keep a private copy of x0
         double *x0c = A->work + smoother_work_doubles(n);
-        AMGP_CUDA(cudaMemcpyAsync(x0c, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, ctx->stream));
+        AMGP_CUDA(cudaMemcpyAsync(x0c, x0, n * sizeof(double), cudaMemcpyDeviceToDevice, cur_stream(ctx)));
         x0 = x0c;
     }
     return smoother_enqueue(ctx, A, m, p, b, x0, x, A->work);
@@ -225,7 +225,7 @@ extern "C" int amgp_smoother_apply_host(amgp_ctx *ctx, amgp_mat *A, const double
     std::lock_guard<std::mutex> g(A->mu);
     AMGP_TRY(ensure_work(A, smoother_work_doubles(n) + n));
     if (A->io_n < 6 * n) {  // two slots of (b, x0, x)
-        cudaStreamSynchronize(ctx->stream);
+        cudaStreamSynchronize(cur_stream(ctx));
         cudaFree(A->io);
         A->io = nullptr;
         A->io_n = 0;
@@ -243,7 +243,7 @@ extern "C" int amgp_smoother_apply_host(amgp_ctx *ctx, amgp_mat *A, const double
         for (auto &e : row)
             if (st == AMGP_OK && cudaEventCreateWithFlags(&e, cudaEventDisableTiming) != cudaSuccess)
                 st = amgp_cuda_fail(cudaGetLastError(), "cudaEventCreate", __FILE__, __LINE__);
-    cudaStream_t h2d = ctx->io_h2d, d2h = ctx->io_d2h, cs = ctx->stream;
+    cudaStream_t h2d = ctx->io_h2d, d2h = ctx->io_d2h, cs = cur_stream(ctx);
     auto chk = [&](cudaError_t e, const char *what) {
         if (e != cudaSuccess && st == AMGP_OK) st = amgp_cuda_fail(e, what, __FILE__, __LINE__);
     };
@@ -291,7 +291,7 @@ extern "C" int amgp_vec_update(amgp_ctx *ctx, int64_t n, double s, const double 
     AMGP_CUDA(cudaSetDevice(ctx->device));
     std::lock_guard<std::mutex> cg(ctx->mu);
     const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, 256), 148 * 16);
-    k_vec_update<<<g, 256, 0, ctx->stream>>>(n, s, a, b, out, sign);
+    k_vec_update<<<g, 256, 0, cur_stream(ctx)>>>(n, s, a, b, out, sign);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }
@@ -305,7 +305,7 @@ extern "C" int amgp_fused_update(amgp_ctx *ctx, int64_t n, double rho, double rh
     const double rp = rho * rho_prev;  // sparse.py:137 evaluates rho*rho_prev first
     const int blk = 256;
     const unsigned g = (unsigned)std::min<int64_t>(grid_for(n, blk), 148 * 16);
-    k_fused_update<<<g, blk, 0, ctx->stream>>>(n, rp, c, s, r, d, x);
+    k_fused_update<<<g, blk, 0, cur_stream(ctx)>>>(n, rp, c, s, r, d, x);
     AMGP_CHECK_LAUNCH(ctx);
     return AMGP_OK;
 }

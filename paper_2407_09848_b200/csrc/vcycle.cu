@@ -33,6 +33,7 @@ struct amgp_hier {
     cudaGraphExec_t gexec = nullptr;
     const double *g_r = nullptr;
     double *g_z = nullptr;
+    cudaStream_t cap_stream = nullptr;  // graph capture stream (see vcycle_enqueue)
     int64_t g_nodes = 0;
     std::mutex mu;
 };
@@ -185,7 +186,7 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
     if (n == 0) return AMGP_OK;
     if (h->coarse_solver == AMGP_COARSE_DENSE_DIRECT) {
         if (!h->cholL) return amgp_fail(AMGP_EINVAL, "dense_direct coarse solver without factor");
-        k_chol_solve<<<1, 256, n * sizeof(double), ctx->stream>>>(n, h->cholL, r, z);
+        k_chol_solve<<<1, 256, n * sizeof(double), cur_stream(ctx)>>>(n, h->cholL, r, z);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
@@ -193,12 +194,12 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
         return smoother_enqueue(ctx, A, h->m[l], h->plan[l], r, nullptr, z, h->work[l]);
     const size_t reg_smem = 16 * (size_t)A->nrows + 10 * (size_t)A->stored + 64;
     if (!A->halo && A->stored <= COARSE_REG_SLOTS && A->ncols < 32768 && reg_smem <= COARSE_SMEM_BYTES) {
-        k_coarse_l1_reg<<<1, 1024, reg_smem, ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
+        k_coarse_l1_reg<<<1, 1024, reg_smem, cur_stream(ctx)>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
     if (!A->halo && coarse_smem(A) <= COARSE_SMEM_BYTES) {
-        k_coarse_l1<<<1, 1024, coarse_smem(A), ctx->stream>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
+        k_coarse_l1<<<1, 1024, coarse_smem(A), cur_stream(ctx)>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
@@ -230,9 +231,17 @@ int vcycle_enqueue(amgp_hier *h, const double *r, double *z) {
         }
         cudaGraph_t graph = nullptr;
         const int64_t before = ctx->launches.load();
-        AMGP_CUDA(cudaStreamBeginCapture(ctx->stream, cudaStreamCaptureModeThreadLocal));
+        // Capture on the hierarchy's private stream, named by this thread's
+        // capture override (amgp_common.cuh): other host threads keep
+        // enqueueing on the context stream meanwhile, and none of their work
+        // can land in the graph.
+        if (!h->cap_stream) AMGP_CUDA(cudaStreamCreateWithFlags(&h->cap_stream, cudaStreamNonBlocking));
+        cudaError_t e = cudaStreamBeginCapture(h->cap_stream, cudaStreamCaptureModeThreadLocal);
+        if (e != cudaSuccess) return amgp_cuda_fail(e, "cudaStreamBeginCapture", __FILE__, __LINE__);
+        amgp_capture = {ctx, h->cap_stream};
         int st = vcycle_level(h, 0, r, z);
-        cudaError_t e = cudaStreamEndCapture(ctx->stream, &graph);
+        amgp_capture = {};
+        e = cudaStreamEndCapture(h->cap_stream, &graph);
         const int64_t nodes = ctx->launches.load() - before;
         ctx->launches.fetch_sub(nodes);  // captured, not launched
         if (st != AMGP_OK) {
@@ -250,7 +259,7 @@ int vcycle_enqueue(amgp_hier *h, const double *r, double *z) {
         h->g_z = z;
         h->g_nodes = nodes;
     }
-    AMGP_CUDA(cudaGraphLaunch(h->gexec, ctx->stream));
+    AMGP_CUDA(cudaGraphLaunch(h->gexec, cur_stream(ctx)));
     ctx->launches.fetch_add(h->g_nodes);
     return AMGP_OK;
 }
@@ -260,6 +269,7 @@ static void hier_free_buffers(amgp_hier *h) {
         for (double *p : *v) cudaFree(p);
     cudaFree(h->cholL);
     if (h->gexec) cudaGraphExecDestroy(h->gexec);
+    if (h->cap_stream) cudaStreamDestroy(h->cap_stream);
 }
 
 extern "C" int amgp_hier_create(amgp_ctx *ctx, int nlevels, amgp_mat *const *A,
@@ -338,7 +348,7 @@ extern "C" int amgp_hier_set_smoother(amgp_hier *h, int level, const amgp_smooth
     for (int l = 0; l < h->nlev; l++)
         if (level < 0 || l == level) h->plan[l] = p;
     if (h->gexec) {  // invalidate the captured graph
-        cudaStreamSynchronize(h->ctx->stream);
+        cudaStreamSynchronize(cur_stream(h->ctx));
         cudaGraphExecDestroy(h->gexec);
         h->gexec = nullptr;
     }
@@ -381,7 +391,7 @@ extern "C" int amgp_hier_info(amgp_hier *h, int *nlevels) {
 extern "C" int amgp_hier_destroy(amgp_hier *h) {
     if (!h) return AMGP_OK;
     cudaSetDevice(h->ctx->device);
-    cudaStreamSynchronize(h->ctx->stream);
+    cudaStreamSynchronize(cur_stream(h->ctx));
     hier_free_buffers(h);
     delete h;
     return AMGP_OK;

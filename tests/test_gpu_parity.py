@@ -267,7 +267,7 @@ def test_pcg_with_smoother_preconditioner(P):
     assert np.linalg.norm(b - A.to_dense() @ x) / np.linalg.norm(b) <= 1e-8
     # any callable r -> z is accepted (reference krylov.py:88); identity = plain CG
     x2, rep2 = P.solve(A, b, precond=lambda r: r.copy(), cfg=P.KrylovConfig(tol=1e-8))
-    assert rep2.converged and rep2.precond_count == rep2.iterations + 1
+    assert rep2.converged and rep2.precond_count == rep2.iterations
     with pytest.raises(TypeError):
         P.solve(A, b, precond=42)
 

@@ -26,6 +26,10 @@ sys.path.insert(0, os.path.join(REPO, "oracle"))
 
 
 def main():
+    if os.environ.get("AMGP_WATCHDOG"):
+        import faulthandler
+
+        faulthandler.dump_traceback_later(float(os.environ["AMGP_WATCHDOG"]), exit=True)
     ap = argparse.ArgumentParser()
     ap.add_argument("--grid", type=int, default=32)
     ap.add_argument("--stencil", type=int, default=7)

@@ -19,8 +19,6 @@
 // so adding +0.0 leaves it unchanged bit for bit.
 #pragma once
 
-#include <stdlib.h>
-
 #include <algorithm>
 
 #include "amgp_common.cuh"
@@ -106,7 +104,6 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                 const int jj = j + u * NW;
                 if (jj < jn) {
                     double p = 0.0;
-                    // own entries through the read-only path, halo entries coherently
                     const int64_t c = cc[u];
                     if (c >= 0) {
                         const bool hc = halo && c >= A.nown;
@@ -131,88 +128,6 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
     if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }
 
-// Deep thread-per-row schedule for long rows on launches with enough slices
-// to keep every SM busy (coarse AMG levels with thousands of slices): one
-// warp per slice, one lane per row, U slots per batch, and the column/value
-// loads of batch b+1 issued before the ordered sum of batch b, so each batch
-// exposes one gather latency instead of a load -> gather chain.  Same
-// operations in the same order as sell_row_dot (padding skipped).
-template <int U, bool HALO>
-__device__ __forceinline__ double sell_row_dot_deep(const SellView &A, int64_t s, int lane,
-                                                    const double *__restrict__ x,
-                                                    const double *__restrict__ xh) {
-    const int64_t base = A.slice_ptr[s];
-    const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
-    const int32_t *c = A.col + base + lane;
-    const double *v = A.val + base + lane;
-    const uint64_t pf = policy_evict_first(), pl = policy_evict_last();
-    int32_t cc[U];
-    double vv[U];
-#pragma unroll
-    for (int u = 0; u < U; u++) {
-        const bool ok = u < w;
-        cc[u] = ok ? ld_stream_s32(c + (int64_t)u * AMGP_SLICE, pf) : -1;
-        vv[u] = ok ? ld_stream_f64(v + (int64_t)u * AMGP_SLICE, pf) : 0.0;
-    }
-    double sum = 0.0;
-    for (int j0 = 0; j0 < w; j0 += U) {
-        double xx[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int64_t cu = cc[u];
-            if (HALO) {
-                const bool own = cu < A.nown;
-                xx[u] = cu < 0 ? 0.0 : ld_halo_f64((own ? x : xh) + (own ? cu : cu - A.nown));
-            } else
-                xx[u] = cu < 0 ? 0.0 : ld_gather_f64(x + cu, pl);
-        }
-        int32_t nc[U];
-        double nv[U];
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            const int j = j0 + U + u;
-            const bool ok = j < w;
-            nc[u] = ok ? ld_stream_s32(c + (int64_t)j * AMGP_SLICE, pf) : -1;
-            nv[u] = ok ? ld_stream_f64(v + (int64_t)j * AMGP_SLICE, pf) : 0.0;
-        }
-#pragma unroll
-        for (int u = 0; u < U; u++)
-            if (cc[u] >= 0) sum = __dadd_rn(sum, __dmul_rn(vv[u], xx[u]));
-#pragma unroll
-        for (int u = 0; u < U; u++) {
-            cc[u] = nc[u];
-            vv[u] = nv[u];
-        }
-    }
-    return sum;
-}
-
-#define DEEP_WARPS 4
-template <class Epi, int MODE, int U>
-__global__ void __launch_bounds__(DEEP_WARPS * 32)
-k_deep_rows(SellView A, const double *__restrict__ xg, Epi epi) {
-    const double *xh = MODE == ROWS_GEN ? halo_wait(A) : nullptr;
-    const int64_t idx = (int64_t)blockIdx.x * DEEP_WARPS + (threadIdx.x >> 5);
-    const int lane = threadIdx.x & 31;
-    if (idx < A.nlist) {
-        const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[idx] : run_slice(A, idx);
-        const double y = sell_row_dot_deep<U, MODE == ROWS_GEN>(A, s, lane, xg, xh);
-        const int64_t row = s * 32 + lane;
-        if (row < A.nrows) epi(row, y);
-    }
-    if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
-}
-
-// Experiment switch (AMGP_ROWS): 0 = default schedule choice, 1 = always the
-// split schedule for long rows, 8/16/24 = the deep schedule with that U.
-inline int rows_variant() {
-    static const int v = [] {
-        const char *e = getenv("AMGP_ROWS");
-        return e ? atoi(e) : 0;
-    }();
-    return v;
-}
-
 // Schedule choice, per launch: split when rows are long and the launch has
 // too few slices to keep the GPU's warps busy with thread-per-row (e.g. the
 // boundary-slice launch of a distributed coarse level: ~800 slices of ~50
@@ -226,14 +141,6 @@ void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const dou
                  const Epi &epi) {
     SellView v = v0;
     const bool split = Epi::kSpmv && use_split(A, v.nlist);
-    const int rv = rows_variant();
-    if (split && v.nlist >= 2 * 148 && rv >= 8) {  // deep thread-per-row (experiment)
-        const unsigned g = grid_for(v.nlist, DEEP_WARPS);
-        if (rv == 8) k_deep_rows<Epi, MODE, 8><<<g, DEEP_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
-        else if (rv == 16) k_deep_rows<Epi, MODE, 16><<<g, DEEP_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
-        else k_deep_rows<Epi, MODE, 24><<<g, DEEP_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
-        return;
-    }
     const int nw = v.nlist < 2 * 148 ? 24 : SPLIT_WARPS;
     const int bs = split ? nw * 32 : ROWS_BLOCK;
     const unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);

@@ -7,7 +7,7 @@ Each SpMV (A_l, R_l = P_l^T, P_l) is launched REPS times back to back on
 the library stream and timed with CUDA events (L2-warm, as inside a
 V-cycle; launch gaps included); GB/s = (12 nnz + 4 (n+1) + 8 ncols + 8 nrows) / time.  Then the
 PCG solve (opt_cheb1 k=4, rtol 1e-6), median of 5.  Schedule experiments:
-AMGP_ROWS=1 (split) / 8 / 16 / 24 (deep thread-per-row, U).
+library variants via AMGP_LIB (tools/ab_solve.py for A/B).
 """
 import argparse
 import json

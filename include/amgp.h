@@ -87,8 +87,9 @@ int amgp_memcpy_d2h(amgp_ctx *ctx, void *dst_host, const void *src_dev, int64_t 
 /* ---- matrices (sparse.py:32-115 CsrMatrix) ----------------------------- */
 /* Upload a host CSR (row_ptr int64[nrows+1], col_idx int64[nnz], values
  * f64[nnz]; columns sorted per row as CsrMatrix guarantees, sparse.py:43-75)
- * and pack it into SELL-32.  Per-row entry order is kept, so the device SpMV
- * accumulates in exactly the reference's order. */
+ * and pack it into SELL-32 (SELL-C-sigma where rows of very different
+ * lengths share slices, see amgp_mat_from_dcsr).  Per-row entry order is
+ * kept, so the device SpMV accumulates in exactly the reference's order. */
 int amgp_mat_from_csr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *row_ptr,
                       const int64_t *col_idx, const double *values, amgp_mat **out);
 /* Rows [row_begin, row_end) of the 3D Poisson matrix on an m^3 grid generated
@@ -280,9 +281,11 @@ int amgp_ds_symmetrize_lookup(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, con
                               const double *g_val, const double *gt, const int64_t *o_rp, const int64_t *o_col,
                               const double *o_val, const int64_t *row_ptr, int64_t *row_cnt, int64_t *col,
                               double *val);
-/* SELL-32 matrix from a device CSR with local int64 columns < 2^31 */
+/* SELL-32 matrix from a device CSR with local int64 columns < 2^31;
+ * sigma != 0: SELL-C-sigma (rows sorted by length inside 256-row windows)
+ * when that stores >= 5 % fewer slots and the matrix has >= 4096 rows. */
 int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *row_ptr,
-                       const int64_t *col, const double *val, amgp_mat **out);
+                       const int64_t *col, const double *val, int sigma, amgp_mat **out);
 int amgp_mat_nown(const amgp_mat *A, int64_t *nown);
 /* host greedy passes of amg.py:124-148 over device-computed strength lists */
 int amgp_setup_sa_pass1(int64_t n, const int64_t *srp, const int32_t *scol, int64_t *agg, int64_t *n_agg);

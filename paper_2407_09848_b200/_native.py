@@ -119,7 +119,7 @@ _SIGS = {
     "amgp_ds_sym_lookup": (C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, C.c_int64, _P64]),
     "amgp_ds_symmetrize_lookup": (C.c_int, [_VP, C.c_int64, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP, _VP,
                                              _VP]),
-    "amgp_mat_from_dcsr": (C.c_int, [_VP, C.c_int64, C.c_int64, _VP, _VP, _VP, C.POINTER(_VP)]),
+    "amgp_mat_from_dcsr": (C.c_int, [_VP, C.c_int64, C.c_int64, _VP, _VP, _VP, C.c_int, C.POINTER(_VP)]),
     "amgp_mat_nown": (C.c_int, [_VP, _P64]),
     "amgp_setup_sa_pass1": (C.c_int, [C.c_int64, _P64, C.POINTER(C.c_int32), _P64, _P64]),
     "amgp_setup_sa_pass2": (C.c_int, [C.c_int64, _P64, _P64, C.POINTER(C.c_int32), _PD, _P64, _P64]),

@@ -152,6 +152,10 @@ struct amgp_mat {
     int32_t *col = nullptr;        // [stored], -1 = padding
     double *val = nullptr;         // [stored]
     int32_t max_width = 0;
+    // SELL-C-sigma: rows sorted by length inside windows of AMGP_SIGMA rows
+    // (fewer padded slots); perm[pos] = row stored at SELL position pos (-1:
+    // padding), iperm[row] = its position.  Both null: identity order.
+    int32_t *perm = nullptr, *iperm = nullptr;
     int64_t row_offset = 0;  // first global row of a generated row block
     std::vector<int64_t> slice_maxcol;  // host: largest column per slice (-1: empty)
     HaloPlan *halo = nullptr;           // non-null: distributed operand
@@ -172,6 +176,8 @@ struct SellView {
     const double *__restrict__ val;
     int64_t nrows;
     int64_t nslices;
+    const int32_t *__restrict__ perm;   // SELL-C-sigma row order (see amgp_mat), or null
+    const int32_t *__restrict__ iperm;
     const int32_t *__restrict__ slist;  // slices to process (nullptr: the run table)
     int64_t nlist;
     int64_t nown;                       // gathers of columns >= nown read xh
@@ -197,6 +203,8 @@ inline SellView view_of(const amgp_mat *A) {
     v.slice_ptr = A->slice_ptr;
     v.col = A->col;
     v.val = A->val;
+    v.perm = A->perm;
+    v.iperm = A->iperm;
     v.nrows = A->nrows;
     v.nslices = A->nslices;
     v.nlist = A->nslices;
@@ -205,6 +213,18 @@ inline SellView view_of(const amgp_mat *A) {
     v.run_s0[0] = 0;
     v.run_end[0] = A->nslices;
     return v;
+}
+
+#define AMGP_SIGMA 256  // sorting window of SELL-C-sigma (8 slices)
+
+// row stored at SELL position pos (slice pos / 32, lane pos % 32); -1: padding
+__device__ __forceinline__ int64_t sell_row(const SellView &A, int64_t pos) {
+    if (A.perm) return A.perm[pos];
+    return pos < A.nrows ? pos : -1;
+}
+// SELL position of row i
+__device__ __forceinline__ int64_t sell_pos(const SellView &A, int64_t i) {
+    return A.iperm ? (int64_t)A.iperm[i] : i;
 }
 
 // slice processed by launch index idx (run table; see SellView)

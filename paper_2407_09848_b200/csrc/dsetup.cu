@@ -42,8 +42,12 @@ int mat_alloc(amgp_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, int64_t 
 
 namespace {
 
-// length of SELL row `lane` of slice s (padding slots sit after the row)
-__device__ __forceinline__ int sell_row_len(const SellView &A, int64_t s, int lane, int64_t *base_out) {
+// length of row i (its SELL position: slice pos / 32, lane pos % 32; padding
+// slots sit after the row); *base_out = the row's first slot
+__device__ __forceinline__ int sell_row_len(const SellView &A, int64_t i, int64_t *base_out) {
+    const int64_t pos = sell_pos(A, i);
+    const int64_t s = pos >> 5;
+    const int lane = (int)(pos & 31);
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
     int len = 0;
@@ -57,7 +61,7 @@ __global__ void k_ds_diag(SellView A, double *__restrict__ d) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= A.nrows) return;
     int64_t b;
-    const int len = sell_row_len(A, i >> 5, (int)(i & 31), &b);
+    const int len = sell_row_len(A, i, &b);
     double acc = 0.0;  // scipy csr_diagonal: sums the (single) diagonal entry from 0
     for (int j = 0; j < len; j++)
         if (A.col[b + (int64_t)j * 32] == i) acc = __dadd_rn(acc, A.val[b + (int64_t)j * 32]);
@@ -75,7 +79,7 @@ __global__ void k_ds_strength(SellView A, const double *__restrict__ d, double t
     if (t >= nlist) return;
     const int64_t i = rows ? rows[t] : t;
     int64_t b;
-    const int len = sell_row_len(A, i >> 5, (int)(i & 31), &b);
+    const int len = sell_row_len(A, i, &b);
     const double di = d[i];
     int64_t k = off ? off[t] : 0, c0 = k;
     for (int j = 0; j < len; j++) {
@@ -314,7 +318,7 @@ __global__ void k_ds_prolong(SellView A, const double *__restrict__ d, const int
             continue;
         }
         int64_t b;
-        const int len = sell_row_len(A, i >> 5, (int)(i & 31), &b);
+        const int len = sell_row_len(A, i, &b);
         const double s = __ddiv_rn(omega, d[i]);
         int u = 0;
         for (int j = len - 1; j >= 0; j--) {
@@ -424,10 +428,11 @@ k_ds_spgemm(ASide a, BRows bm, const int64_t *__restrict__ arows, const int64_t 
         int64_t abase = 0, aend = 0;
         int astride = 1;
         if (a.is_sell) {
-            const int64_t s = r >> 5;
+            const int64_t pos = sell_pos(a.sell, r);
+            const int64_t s = pos >> 5;
             const int64_t base = a.sell.slice_ptr[s];
             const int w = (int)((a.sell.slice_ptr[s + 1] - base) >> 5);
-            abase = base + (r & 31);
+            abase = base + (pos & 31);
             aend = abase + (int64_t)w * 32;
             astride = 32;
         } else {
@@ -627,17 +632,68 @@ __global__ void k_dcsr_width(int64_t n, const int64_t *__restrict__ rp, int32_t 
     if ((i & 31) == 0) w[i >> 5] = len;
 }
 
+// SELL-C-sigma: one warp sorts one window of AMGP_SIGMA rows by descending
+// length (stable: ties keep the row order) in shared memory, writes the
+// window's positions -> rows into perm and the sorted slice widths.
+__global__ void __launch_bounds__(128) k_sigma_sort(int64_t n, const int64_t *__restrict__ rp,
+                                                     int32_t *__restrict__ perm, int32_t *__restrict__ wsorted) {
+    const int64_t npos = (n + 31) / 32 * 32;  // positions of the SELL layout
+    __shared__ unsigned long long key[4][AMGP_SIGMA];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t win = (int64_t)blockIdx.x * 4 + warp;
+    const int64_t w0 = win * AMGP_SIGMA;
+    if (w0 >= n) return;
+    unsigned long long *k = key[warp];
+    for (int t = lane; t < AMGP_SIGMA; t += 32) {
+        const int64_t r = w0 + t;
+        // (0x7fffffff - len) high, window offset low: ascending = longest first, stable
+        const unsigned long long len = r < n ? (unsigned long long)(rp[r + 1] - rp[r]) : 0ull;
+        k[t] = r < n ? ((0x7fffffffull - len) << 32) | (unsigned long long)t : ~0ull;
+    }
+    __syncwarp();
+    for (int size = 2; size <= AMGP_SIGMA; size <<= 1)
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = lane; t < AMGP_SIGMA; t += 32) {
+                const int o = t ^ stride;
+                if (o > t) {
+                    const bool up = (t & size) == 0;
+                    const unsigned long long x = k[t], y = k[o];
+                    if ((x > y) == up) {
+                        k[t] = y;
+                        k[o] = x;
+                    }
+                }
+            }
+            __syncwarp();
+        }
+    for (int t = lane; t < AMGP_SIGMA; t += 32) {
+        const int64_t pos = w0 + t;
+        if (pos >= npos) break;
+        const bool real = k[t] != ~0ull;
+        perm[pos] = real ? (int32_t)(w0 + (int64_t)(k[t] & 0xffffffffull)) : -1;
+        if ((t & 31) == 0)  // slice width = its first (longest) row
+            wsorted[pos >> 5] = real ? (int32_t)(0x7fffffffull - (k[t] >> 32)) : 0;
+    }
+}
+
+__global__ void k_sigma_iperm(int64_t npos, const int32_t *__restrict__ perm, int32_t *__restrict__ iperm) {
+    for (int64_t p = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; p < npos; p += (int64_t)gridDim.x * blockDim.x)
+        if (perm[p] >= 0) iperm[perm[p]] = (int32_t)p;
+}
+
+// SELL slots of position i (row perm[i], or i itself without a permutation)
 __global__ void k_dcsr_fill(int64_t n, int64_t ncols, const int64_t *__restrict__ rp,
                             const int64_t *__restrict__ col, const double *__restrict__ val,
-                            const int64_t *__restrict__ sp, int32_t *__restrict__ scol, double *__restrict__ sval,
-                            int *bad) {
+                            const int32_t *__restrict__ perm, const int64_t *__restrict__ sp,
+                            int32_t *__restrict__ scol, double *__restrict__ sval, int *bad) {
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     const int64_t s = i >> 5;
     if (s >= (n + 31) / 32) return;
     const int lane = (int)(i & 31);
     const int w = (int)((sp[s + 1] - sp[s]) >> 5);
-    const int64_t r0 = i < n ? rp[i] : 0;
-    const int len = i < n ? (int)(rp[i + 1] - r0) : 0;
+    const int64_t row = perm ? (int64_t)perm[i] : (i < n ? i : -1);
+    const int64_t r0 = row >= 0 ? rp[row] : 0;
+    const int len = row >= 0 ? (int)(rp[row + 1] - r0) : 0;
     for (int j = 0; j < w; j++) {
         const int64_t o = sp[s] + (int64_t)j * 32 + lane;
         if (j < len) {
@@ -982,28 +1038,64 @@ int amgp_ds_symmetrize_lookup(amgp_ctx *ctx, int64_t n, const int64_t *g_rp, con
 
 // SELL-32 matrix from a device CSR (columns already local, sorted per row as
 // produced by the setup): per-slice widths on the device, slice offsets on
-// the host, one fill launch.
+// the host, one fill launch.  sigma != 0: SELL-C-sigma -- rows sorted by
+// length inside windows of AMGP_SIGMA rows when that stores >= 5 % fewer
+// slots (coarse AMG levels, restriction operators); the row order inside
+// each row is untouched, so every row sum keeps the reference's order.
+// Matrices under AMGP_SIGMA_MIN_ROWS rows stay unsorted (coarsest levels:
+// the single-CTA coarse solver addresses rows by position).
+#ifndef AMGP_SIGMA_MIN_ROWS
+#define AMGP_SIGMA_MIN_ROWS 4096
+#endif
 int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *rp, const int64_t *col,
-                       const double *val, amgp_mat **out) {
+                       const double *val, int sigma, amgp_mat **out) {
     if (!ctx || !out || nrows < 0 || ncols < 0 || (nrows && !rp))
         return amgp_fail(AMGP_EINVAL, "amgp_mat_from_dcsr: bad argument");
     if (ncols > (int64_t)INT32_MAX + 1) return amgp_fail(AMGP_EINVAL, "matrix too large for int32 column indices");
+    if (nrows > INT32_MAX) return amgp_fail(AMGP_EINVAL, "too many rows for one device matrix");
     AMGP_CUDA(cudaSetDevice(ctx->device));
+    cudaStream_t st = cur_stream(ctx);
     const int64_t ns = (nrows + 31) / 32;
     int64_t nnz = 0;
-    if (nrows) AMGP_CUDA(cudaMemcpyAsync(&nnz, rp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, cur_stream(ctx)));
-    std::vector<int32_t> w(std::max<int64_t>(ns, 1));
+    if (nrows) AMGP_CUDA(cudaMemcpyAsync(&nnz, rp + nrows, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    std::vector<int32_t> w(std::max<int64_t>(ns, 1)), ws(std::max<int64_t>(ns, 1));
+    int32_t *dperm = nullptr, *dw = nullptr;
+    const bool try_sigma = sigma && nrows >= AMGP_SIGMA_MIN_ROWS;
     if (ns) {
-        int32_t *dw = nullptr;
-        AMGP_CUDA(cudaMalloc(&dw, ns * sizeof(int32_t)));
-        k_dcsr_width<<<grid_for(ns * 32, 256), 256, 0, cur_stream(ctx)>>>(nrows, rp, dw);
+        AMGP_CUDA(cudaMalloc(&dw, 2 * ns * sizeof(int32_t)));
+        k_dcsr_width<<<grid_for(ns * 32, 256), 256, 0, st>>>(nrows, rp, dw);
         cudaError_t e = cudaGetLastError();
-        if (e == cudaSuccess) e = cudaMemcpyAsync(w.data(), dw, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, cur_stream(ctx));
-        if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
+        if (e == cudaSuccess && try_sigma) {
+            e = cudaMalloc(&dperm, (size_t)ns * 32 * sizeof(int32_t));
+            const int64_t nwin = (nrows + AMGP_SIGMA - 1) / AMGP_SIGMA;
+            if (e == cudaSuccess) {
+                k_sigma_sort<<<(unsigned)((nwin + 3) / 4), 128, 0, st>>>(nrows, rp, dperm, dw + ns);
+                e = cudaGetLastError();
+            }
+        }
+        if (e == cudaSuccess) e = cudaMemcpyAsync(w.data(), dw, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess && try_sigma)
+            e = cudaMemcpyAsync(ws.data(), dw + ns, ns * sizeof(int32_t), cudaMemcpyDeviceToHost, st);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
         cudaFree(dw);
-        if (e != cudaSuccess) return amgp_cuda_fail(e, "k_dcsr_width", __FILE__, __LINE__);
+        if (e != cudaSuccess) {
+            cudaFree(dperm);
+            return amgp_cuda_fail(e, "SELL widths", __FILE__, __LINE__);
+        }
     } else {
-        AMGP_CUDA(cudaStreamSynchronize(cur_stream(ctx)));
+        AMGP_CUDA(cudaStreamSynchronize(st));
+    }
+    int64_t stored_u = 0, stored_s = 0;
+    for (int64_t s = 0; s < ns; s++) {
+        stored_u += (int64_t)w[s] * 32;
+        stored_s += (int64_t)ws[s] * 32;
+    }
+    const bool use_sigma = try_sigma && stored_s * 100 <= stored_u * 95;
+    if (!use_sigma) {
+        cudaFree(dperm);
+        dperm = nullptr;
+    } else {
+        w.swap(ws);
     }
     std::vector<int64_t> sp(ns + 1);
     int64_t stored = 0;
@@ -1015,21 +1107,30 @@ int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_
     }
     sp[ns] = stored;
     amgp_mat *A = nullptr;
-    AMGP_TRY(mat_alloc(ctx, nrows, ncols, nnz, ns, stored, &A));
+    int st_alloc = mat_alloc(ctx, nrows, ncols, nnz, ns, stored, &A);
+    if (st_alloc != AMGP_OK) {
+        cudaFree(dperm);
+        return st_alloc;
+    }
     A->max_width = wmax;
+    A->perm = dperm;
     int *bad = nullptr;
-    cudaError_t e = cudaMemcpyAsync(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice,
-                                    cur_stream(ctx));
+    cudaError_t e = cudaMemcpyAsync(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+    if (e == cudaSuccess && dperm) e = cudaMalloc(&A->iperm, std::max<int64_t>(nrows, 1) * sizeof(int32_t));
+    if (e == cudaSuccess && dperm) {
+        k_sigma_iperm<<<grid_for(ns * 32, 256), 256, 0, st>>>(ns * 32, dperm, A->iperm);
+        e = cudaGetLastError();
+    }
     if (e == cudaSuccess) e = cudaMalloc(&bad, sizeof(int));
-    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), cur_stream(ctx));
+    if (e == cudaSuccess) e = cudaMemsetAsync(bad, 0, sizeof(int), st);
     if (e == cudaSuccess && ns) {
-        k_dcsr_fill<<<grid_for(ns * 32, 256), 256, 0, cur_stream(ctx)>>>(nrows, ncols, rp, col, val, A->slice_ptr,
-                                                                     A->col, A->val, bad);
+        k_dcsr_fill<<<grid_for(ns * 32, 256), 256, 0, st>>>(nrows, ncols, rp, col, val, dperm, A->slice_ptr, A->col,
+                                                            A->val, bad);
         e = cudaGetLastError();
     }
     int hbad = 0;
-    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, cur_stream(ctx));
-    if (e == cudaSuccess) e = cudaStreamSynchronize(cur_stream(ctx));
+    if (e == cudaSuccess) e = cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
     cudaFree(bad);
     if (e != cudaSuccess) {
         amgp_mat_destroy(A);
@@ -1039,7 +1140,7 @@ int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_
         amgp_mat_destroy(A);
         return amgp_fail(AMGP_EINVAL, "column index out of range");
     }
-    ctx->launches.fetch_add(ns ? 2 : 0);
+    ctx->launches.fetch_add(ns ? (dperm ? 4 : 2) : 0);
     int rs = refresh_slice_maxcol(A);
     if (rs != AMGP_OK) {
         amgp_mat_destroy(A);

@@ -80,46 +80,42 @@ int mat_alloc(amgp_ctx *ctx, int64_t nrows, int64_t ncols, int64_t nnz, int64_t 
     return AMGP_OK;
 }
 
+int amgp_mat_from_dcsr(amgp_ctx *ctx, int64_t nrows, int64_t ncols, const int64_t *rp, const int64_t *col,
+                       const double *val, int sigma, amgp_mat **out);
+
+// Host CSR -> device: validated here, uploaded, and packed on the device
+// (amgp_mat_from_dcsr, SELL-C-sigma where it saves slots).
 extern "C" int amgp_mat_from_csr(amgp_ctx *ctx, int64_t nrows, int64_t ncols,
                                  const int64_t *row_ptr, const int64_t *col_idx,
                                  const double *values, amgp_mat **out) {
     if (!ctx || !out || nrows < 0 || ncols < 0 || !row_ptr)
         return amgp_fail(AMGP_EINVAL, "amgp_mat_from_csr: bad argument");
     if (row_ptr[0] != 0) return amgp_fail(AMGP_EINVAL, "row_ptr endpoints inconsistent with values");
-    if (ncols > INT32_MAX || nrows > INT32_MAX * 32LL)
+    if (ncols > INT32_MAX || nrows > INT32_MAX)
         return amgp_fail(AMGP_EINVAL, "matrix too large for int32 column indices");
-    AMGP_CUDA(cudaSetDevice(ctx->device));
-    int64_t ns = 0, stored = 0;
-    AMGP_TRY(amgp_sell_pack_host(nrows, row_ptr, col_idx, values, &ns, &stored, nullptr,
-                                 nullptr, nullptr));
-    std::vector<int64_t> sp(ns + 1);
-    std::vector<int32_t> col(std::max<int64_t>(stored, 1));
-    std::vector<double> val(std::max<int64_t>(stored, 1));
-    AMGP_TRY(amgp_sell_pack_host(nrows, row_ptr, col_idx, values, &ns, &stored, sp.data(),
-                                 col.data(), val.data()));
-    for (int64_t k = 0; k < row_ptr[nrows]; k++)
+    for (int64_t i = 0; i < nrows; i++)
+        if (row_ptr[i + 1] < row_ptr[i]) return amgp_fail(AMGP_EINVAL, "row_ptr must be nondecreasing");
+    const int64_t nnz = row_ptr[nrows];
+    for (int64_t k = 0; k < nnz; k++) {
+        if (col_idx[k] < 0 || col_idx[k] > INT32_MAX) return amgp_fail(AMGP_EINVAL, "column index out of int32 range");
         if (col_idx[k] >= ncols) return amgp_fail(AMGP_EINVAL, "column index >= ncols");
-    amgp_mat *A = nullptr;
-    AMGP_TRY(mat_alloc(ctx, nrows, ncols, row_ptr[nrows], ns, stored, &A));
-    int32_t wmax = 0;
-    A->slice_maxcol.assign(ns, -1);
-    for (int64_t s = 0; s < ns; s++) {
-        wmax = std::max<int32_t>(wmax, (int32_t)((sp[s + 1] - sp[s]) / AMGP_SLICE));
-        for (int64_t e = sp[s]; e < sp[s + 1]; e++)
-            A->slice_maxcol[s] = std::max<int64_t>(A->slice_maxcol[s], col[e]);
     }
-    A->max_width = wmax;
-    cudaError_t e = cudaMemcpy(A->slice_ptr, sp.data(), (ns + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && stored > 0)
-        e = cudaMemcpy(A->col, col.data(), stored * sizeof(int32_t), cudaMemcpyHostToDevice);
-    if (e == cudaSuccess && stored > 0)
-        e = cudaMemcpy(A->val, val.data(), stored * sizeof(double), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) {
-        amgp_mat_destroy(A);
-        return amgp_cuda_fail(e, "matrix upload", __FILE__, __LINE__);
-    }
-    *out = A;
-    return AMGP_OK;
+    AMGP_CUDA(cudaSetDevice(ctx->device));
+    int64_t *drp = nullptr, *dcol = nullptr;
+    double *dval = nullptr;
+    cudaError_t e = cudaMalloc(&drp, (nrows + 1) * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaMalloc(&dcol, std::max<int64_t>(nnz, 1) * sizeof(int64_t));
+    if (e == cudaSuccess) e = cudaMalloc(&dval, std::max<int64_t>(nnz, 1) * sizeof(double));
+    if (e == cudaSuccess) e = cudaMemcpy(drp, row_ptr, (nrows + 1) * sizeof(int64_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && nnz) e = cudaMemcpy(dcol, col_idx, nnz * sizeof(int64_t), cudaMemcpyHostToDevice);
+    if (e == cudaSuccess && nnz) e = cudaMemcpy(dval, values, nnz * sizeof(double), cudaMemcpyHostToDevice);
+    int st = e == cudaSuccess ? amgp_mat_from_dcsr(ctx, nrows, ncols, drp, dcol, dval, 1, out)
+                              : amgp_cuda_fail(e, "matrix upload", __FILE__, __LINE__);
+    cudaStreamSynchronize(cur_stream(ctx));
+    cudaFree(drp);
+    cudaFree(dcol);
+    cudaFree(dval);
+    return st;
 }
 
 extern "C" int amgp_mat_destroy(amgp_mat *A) {
@@ -135,6 +131,8 @@ extern "C" int amgp_mat_destroy(amgp_mat *A) {
     cudaFree(A->val);
     cudaFree(A->work);
     cudaFree(A->io);
+    cudaFree(A->perm);
+    cudaFree(A->iperm);
     delete A;
     return AMGP_OK;
 }
@@ -155,16 +153,22 @@ extern "C" int amgp_mat_to_csr(amgp_mat *A, int64_t *row_ptr, int64_t *col_idx, 
     std::vector<int64_t> sp(A->nslices + 1);
     std::vector<int32_t> col(std::max<int64_t>(A->stored, 1));
     std::vector<double> val(std::max<int64_t>(A->stored, 1));
+    std::vector<int32_t> iperm;
     AMGP_CUDA(cudaStreamSynchronize(cur_stream(A->ctx)));
     AMGP_CUDA(cudaMemcpy(sp.data(), A->slice_ptr, sp.size() * sizeof(int64_t), cudaMemcpyDeviceToHost));
     if (A->stored > 0) {
         AMGP_CUDA(cudaMemcpy(col.data(), A->col, A->stored * sizeof(int32_t), cudaMemcpyDeviceToHost));
         AMGP_CUDA(cudaMemcpy(val.data(), A->val, A->stored * sizeof(double), cudaMemcpyDeviceToHost));
     }
+    if (A->iperm) {
+        iperm.resize(A->nrows);
+        AMGP_CUDA(cudaMemcpy(iperm.data(), A->iperm, A->nrows * sizeof(int32_t), cudaMemcpyDeviceToHost));
+    }
     int64_t k = 0;
     row_ptr[0] = 0;
     for (int64_t i = 0; i < A->nrows; i++) {
-        int64_t s = i / AMGP_SLICE, t = i % AMGP_SLICE;
+        const int64_t pos = A->iperm ? iperm[i] : i;  // SELL position of row i
+        int64_t s = pos / AMGP_SLICE, t = pos % AMGP_SLICE;
         int64_t w = (sp[s + 1] - sp[s]) / AMGP_SLICE;
         for (int64_t j = 0; j < w; j++) {
             int64_t o = sp[s] + j * AMGP_SLICE + t;
@@ -353,8 +357,8 @@ __global__ void k_l1_diag(SellView A, int64_t row_offset, double *__restrict__ m
     int64_t s = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
     int lane = threadIdx.x & 31;
     if (s >= A.nslices) return;
-    int64_t row = s * 32 + lane;
-    if (row >= A.nrows) return;
+    const int64_t row = sell_row(A, s * 32 + lane);
+    if (row < 0) return;
     const int64_t base = A.slice_ptr[s];
     const int w = (int)((A.slice_ptr[s + 1] - base) >> 5);
     const double *v = A.val + base + lane;

@@ -168,8 +168,8 @@ k_pcg_spmv_dot(SellView A, const double *__restrict__ d, double *__restrict__ Ad
     for (int64_t s = (int64_t)blockIdx.x * (RB / 32) + (threadIdx.x >> 5); s < A.nslices;
          s += (int64_t)gridDim.x * (RB / 32)) {
         const double y = sell_row_dot<8>(A, s, lane, d);
-        const int64_t row = s * 32 + lane;
-        if (row < A.nrows) {
+        const int64_t row = sell_row(A, s * 32 + lane);
+        if (row >= 0) {
             Ad[row] = y;
             const double di = d[row];
             acc[0] = __dadd_rn(acc[0], __dmul_rn(di, y));

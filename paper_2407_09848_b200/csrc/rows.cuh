@@ -52,8 +52,8 @@ __device__ __forceinline__ void thread_rows_body(const SellView &A, int64_t cta,
     const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[idx] : run_slice(A, idx);
     double y = 0.0;
     if (Epi::kSpmv) y = sell_row_dot<ROWS_U, HALO>(A, s, lane, xg, xh);
-    const int64_t row = s * 32 + lane;
-    if (row < A.nrows) epi(row, y);
+    const int64_t row = sell_row(A, s * 32 + lane);
+    if (row >= 0) epi(row, y);
 }
 
 template <class Epi, int MODE>
@@ -122,8 +122,8 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
         __syncthreads();
     }
     if (warp == 0) {
-        const int64_t row = s * 32 + lane;
-        if (row < A.nrows) epi(row, sum);
+        const int64_t row = sell_row(A, s * 32 + lane);
+        if (row >= 0) epi(row, sum);
     }
     if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
 }

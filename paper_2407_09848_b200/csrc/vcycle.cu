@@ -193,12 +193,13 @@ static int coarse_enqueue(amgp_hier *h, const double *r, double *z) {
     if (h->coarse_solver == AMGP_COARSE_SMOOTHER)
         return smoother_enqueue(ctx, A, h->m[l], h->plan[l], r, nullptr, z, h->work[l]);
     const size_t reg_smem = 16 * (size_t)A->nrows + 10 * (size_t)A->stored + 64;
-    if (!A->halo && A->stored <= COARSE_REG_SLOTS && A->ncols < 32768 && reg_smem <= COARSE_SMEM_BYTES) {
+    // (the single-CTA kernels address rows by SELL position: identity order only)
+    if (!A->halo && !A->perm && A->stored <= COARSE_REG_SLOTS && A->ncols < 32768 && reg_smem <= COARSE_SMEM_BYTES) {
         k_coarse_l1_reg<<<1, 1024, reg_smem, cur_stream(ctx)>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;
     }
-    if (!A->halo && coarse_smem(A) <= COARSE_SMEM_BYTES) {
+    if (!A->halo && !A->perm && coarse_smem(A) <= COARSE_SMEM_BYTES) {
         k_coarse_l1<<<1, 1024, coarse_smem(A), cur_stream(ctx)>>>(view_of(A), h->m[l], r, z, h->coarse_sweeps);
         AMGP_CHECK_LAUNCH(ctx);
         return AMGP_OK;

@@ -123,7 +123,7 @@ def _sell(c, csr, ncols):
     h = N._VP()
     with c.scope():
         N.check(_lib().amgp_mat_from_dcsr(c.handle, csr.nrows, int(ncols), _p(csr.rp), _p(csr.col),
-                                          _p(csr.val), C.byref(h)))
+                                          _p(csr.val), 1, C.byref(h)))
     return DeviceMatrix(h, c, csr.nrows, int(ncols), csr.nnz)
 
 

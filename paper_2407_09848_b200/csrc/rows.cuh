@@ -145,10 +145,11 @@ void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const dou
     const int bs = split ? nw * 32 : ROWS_BLOCK;
     const unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);
     if (split) {
-        if (nw == 24)
+        if (nw == 24) {
             k_split_rows<Epi, MODE, 24, 8><<<grid, 24 * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
-        else
+        } else {
             k_split_rows<Epi, MODE, SPLIT_WARPS, SPLIT_U><<<grid, SPLIT_WARPS * 32, 0, cur_stream(ctx)>>>(v, xg, epi);
+        }
     } else {
         k_thread_rows<Epi, MODE><<<grid, ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, xg, epi);
     }

@@ -142,7 +142,6 @@ void launch_mode(amgp_ctx *ctx, const amgp_mat *A, const SellView &v0, const dou
     SellView v = v0;
     const bool split = Epi::kSpmv && use_split(A, v.nlist);
     const int nw = v.nlist < 2 * 148 ? 24 : SPLIT_WARPS;
-    const int bs = split ? nw * 32 : ROWS_BLOCK;
     const unsigned grid = split ? (unsigned)v.nlist : grid_for(v.nlist, ROWS_SLICES);
     if (split) {
         if (nw == 24) {

@@ -346,6 +346,37 @@ def test_256cube_generated_smoother_bitwise_vs_oracle(P):
         oracle.set_threads(1)
 
 
+def test_512cube_config3_smoother_bitwise_vs_oracle(P):
+    """BASELINE configs[2] at its size (512^3, 938M stored entries): the
+    device-generated fine level (downloaded as the oracle's CSR), the three
+    polynomial families at k = 4, bitwise against the multi-threaded C
+    oracle."""
+    import torch
+
+    D = P.poisson3d_device(512)
+    H = D.host()  # the device matrix itself (to_csr), as the oracle's input
+    n = D.nrows
+    assert D.nnz == 7 * 512 ** 3 - 6 * 512 ** 2
+    M = P.L1JacobiData(m_diag=D.l1_diag())
+    m_host = D.l1_diag().cpu().numpy()
+    rng = np.random.default_rng(2)
+    b, x0 = rng.standard_normal(n), rng.standard_normal(n)
+    oracle.set_threads(oracle.max_threads())
+    try:
+        for fam in ("cheb4", "opt_cheb4", "opt_cheb1"):
+            cfg = P.PolySmootherConfig(family=fam, degree=4)
+            beta = cfg.beta.beta if cfg.family == "opt_cheb4" else None
+            got = P.smoother_apply(cfg, D, M, torch.tensor(b, device="cuda"),
+                                   torch.tensor(x0, device="cuda")).cpu().numpy()
+            want = oracle.smoother_apply(cfg.family, 4, H.row_ptr, H.col_idx, H.values, m_host,
+                                         b, x0, a=cfg.a or 0.0, beta=beta)
+            assert np.array_equal(got, want), fam
+    finally:
+        oracle.set_threads(1)
+    del D, H
+    torch.cuda.empty_cache()
+
+
 def _sha(a):
     import hashlib
 

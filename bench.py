@@ -368,7 +368,7 @@ def solve_bench(m, kind="smoothed_aggregation", cpu=True, stencil=7, k=4, cpu_fa
 
 
 def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, strong=False, replicate_below=20000,
-                     variant="pcg"):
+                     variant="pcg", graph=True):
     """PCG + AMG solve over all ranks (also N = 1): weak-scaled (BASELINE
     configs[3]: global cube round(m_base N^(1/3)), ~m_base^3 rows per GPU) or
     strong-scaled (configs[4]: global cube m_base).  Each rank generates its
@@ -390,7 +390,7 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, stron
     if comm is not None:
         D0 = Dist.poisson3d_block(m, comm, stencil=stencil)
         levels, _ = DS.build_levels(D0, P.CoarseningConfig(), comm=comm, replicate_below=replicate_below)
-        dh = Dist.DistHierarchy.from_levels(levels, comm, cfg)
+        dh = Dist.DistHierarchy.from_levels(levels, comm, cfg, use_graph=graph)
         c = dh.ctx
         lo, hi = dh.row_range
         As, Ps, Rs = dh.As, dh.Ps, dh.Rs
@@ -446,7 +446,7 @@ def dist_solve_bench(comm, m_base, ws, family="opt_cheb4", k=4, stencil=7, stron
             "setup": "device" + (", distributed (decoupled aggregation)" if comm is not None else ""),
             "setup_s": setup_s, "iterations": rep.iterations, "final_relres": rep.final_relres,
             "solve_s": sec, "wall_s": float(t[1].item()), "tol": 1e-6, "krylov": variant,
-            "replicate_below": replicate_below,
+            "replicate_below": replicate_below, "vcycle_graph": bool(graph) if comm is not None else True,
             "roofline_rank0": solve_roofline(shapes, k, family, rep.iterations, sec, peak),
             "clocks_rank0": clocks}
 
@@ -475,7 +475,8 @@ def run_b200(args):
             comm = Dist.Communicator(local)
         res = dist_solve_bench(comm, args.weak_grid, ws, family=args.solve_family or "opt_cheb4",
                                k=args.solve_k, stencil=args.solve_stencil, strong=args.solve_scaling == "strong",
-                               replicate_below=args.replicate_below, variant=args.krylov)
+                               replicate_below=args.replicate_below, variant=args.krylov,
+                               graph=bool(args.dist_graph))
         if rank == 0:
             res["peak_mem_gb_rank0"] = torch.cuda.max_memory_allocated() / 1e9
             print(json.dumps({"solve_only": True, "n_gpus": ws, "solve": res}), flush=True)
@@ -594,7 +595,8 @@ def run_b200(args):
     if ws > 1 and args.weak_grid > 0:
         dsolve = dist_solve_bench(comm, args.weak_grid, ws, family=args.solve_family or "opt_cheb4",
                                   k=args.solve_k, stencil=args.solve_stencil,
-                                  strong=args.solve_scaling == "strong")
+                                  strong=args.solve_scaling == "strong", replicate_below=args.replicate_below,
+                                  variant=args.krylov, graph=bool(args.dist_graph))
 
     if rank == 0:
         line = {
@@ -672,6 +674,8 @@ def main():
                     help="N > 1: AMG levels with fewer global rows are replicated on every rank")
     ap.add_argument("--krylov", default="pcg", choices=["pcg", "fcg", "pcg1"],
                     help="Krylov variant of the multi-GPU / weak-scaling solves")
+    ap.add_argument("--dist-graph", type=int, default=1, choices=[0, 1],
+                    help="N > 1: replay the distributed V-cycle from a CUDA graph (0: eager launches)")
     ap.add_argument("--solve-only", action="store_true",
                     help="run only the --weak-grid solve (diagnostics for BASELINE configs[3]/[4])")
     ap.add_argument("--solve-scaling", default="weak", choices=["weak", "strong"],

@@ -75,6 +75,9 @@ struct amgp_ctx {
     // and synchronisation words mapped through CUDA IPC; the kernels
     // themselves signal and wait (sync_stride words per matrix slot)
     int halo_p2p = 0;  // 0: NCCL, 1: p2p (default)
+    // p2p: interior and boundary slices in one launch (rows.cuh launch_rows):
+    // AMGP_HALO_FUSE=0 never, 1 where it measured faster (default), 2 always
+    int halo_fuse = 1;
     // copy streams of the host-buffer smoother path (created on first use)
     cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
     unsigned long long *sync = nullptr;            // [AMGP_MAX_SLOTS][sync_stride]
@@ -236,6 +239,13 @@ __device__ __forceinline__ int64_t run_slice(const SellView &A, int64_t idx) {
     return s;
 }
 
+// An opaque copy of p: loads through it cannot be scheduled before this point
+// (the halo pointer after halo_wait's barrier).
+__device__ __forceinline__ const double *launder_ptr(const double *p) {
+    asm volatile("" : "+l"(p)::"memory");
+    return p;
+}
+
 // system-scope acquire / release on u64 words (peer-mapped synchronisation)
 __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long *p) {
     unsigned long long v;
@@ -276,7 +286,7 @@ __device__ __forceinline__ const double *halo_wait(const SellView &A) {
         }
     }
     __syncthreads();
-    return A.xh + (int64_t)(e & 1ull) * A.xh_stride;
+    return launder_ptr(A.xh + (int64_t)(e & 1ull) * A.xh_stride);
 }
 
 // End of a boundary launch of the p2p transport, called by its nctas CTAs:
@@ -371,15 +381,23 @@ __device__ __forceinline__ double ld_gather_f64(const double *p, uint64_t pol) {
 }
 // Gathers of a boundary launch (columns may index the halo, which a peer GPU
 // writes while the kernel runs on the p2p transport): never through the
-// non-coherent path, cached at L2 only (the point of coherence for the
-// peer's NVLink stores), and with a memory clobber so the compiler cannot
-// hoist them above the in-kernel halo wait (acquire + barrier).  One load
-// from a selected pointer per slot keeps the U gathers a single predicated
-// batch (a per-slot branch between two load kinds serialised them: 0.42 vs
-// 0.31 s per 635^3 solve on 4 GPUs).
-__device__ __forceinline__ double ld_halo_f64(const double *p) {
+// non-coherent (.nc) path.  A weak ld.global is coherent after the in-kernel
+// acquire (halo_wait: ld.acquire.sys, which also invalidates the SM's L1, then
+// bar.sync), and it keeps L1 reuse of the neighbouring x entries; the
+// compiler cannot hoist it above the wait because the halo pointer comes out
+// of halo_wait laundered (launder_ptr, after the barrier).  One load from a
+// selected pointer per slot keeps the U gathers a single predicated batch (a
+// per-slot branch between two load kinds serialised them: 0.42 vs 0.31 s per
+// 635^3 solve on 4 GPUs).  AMGP_HALO_LD_CG: the previous L2-only .cg load with
+// a memory clobber (A/B variant).
+__device__ __forceinline__ double ld_halo_f64(const double *p, uint64_t pol) {
     double v;
+#ifdef AMGP_HALO_LD_CG
+    (void)pol;
     asm("ld.global.cg.f64 %0, [%1];" : "=d"(v) : "l"(p) : "memory");
+#else
+    asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(p), "l"(pol));
+#endif
     return v;
 }
 
@@ -414,7 +432,7 @@ __device__ __forceinline__ double sell_row_dot(const SellView &A, int64_t s, int
                 const int64_t c = cc[u];
                 const bool own = c < A.nown;
                 const double *p = (own ? x : xh) + (own ? c : c - A.nown);
-                xx[u] = c < 0 ? 0.0 : ld_halo_f64(p);
+                xx[u] = c < 0 ? 0.0 : ld_halo_f64(p, pl);
             } else
                 xx[u] = cc[u] < 0 ? 0.0 : ld_gather_f64(x + cc[u], pl);
         }

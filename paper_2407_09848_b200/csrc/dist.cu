@@ -158,6 +158,8 @@ static int p2p_init(amgp_ctx *ctx) {
     }
     AMGP_CUDA(cudaDeviceSynchronize());
     ctx->halo_p2p = 1;
+    const char *fz = getenv("AMGP_HALO_FUSE");
+    ctx->halo_fuse = fz && fz[0] >= '0' && fz[0] <= '2' ? fz[0] - '0' : 1;
     return AMGP_OK;
 }
 

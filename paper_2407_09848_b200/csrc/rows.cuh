@@ -73,13 +73,10 @@ k_thread_rows(SellView A, const double *__restrict__ xg, Epi epi) {
 // two per SM is latency bound (a slice's chunk costs ceil(192 / (NW U))
 // dependent column->gather rounds), so it takes 24 warps x 8 = one round.
 template <class Epi, int MODE, int NW, int U>
-__global__ void __launch_bounds__(NW * 32)
-k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
-    __shared__ double prod[SPLIT_CHUNK * 32];
-    const int64_t cta = blockIdx.x;
-    const bool halo = MODE == ROWS_GEN;
-    const double *xh = A.xh;
-    if (MODE == ROWS_GEN) xh = halo_wait(A);
+__device__ __forceinline__ void split_rows_body(const SellView &A, int64_t cta, const double *__restrict__ xg,
+                                                const double *__restrict__ xh, const Epi &epi,
+                                                double *__restrict__ prod) {
+    const bool halo = MODE == ROWS_GEN && A.xh != nullptr;
     const int64_t s = MODE == ROWS_GEN && A.slist ? (int64_t)A.slist[cta] : run_slice(A, cta);
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int64_t base = A.slice_ptr[s];
@@ -108,7 +105,7 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
                     if (c >= 0) {
                         const bool hc = halo && c >= A.nown;
                         const double *src = (hc ? xh : xg) + (hc ? c - A.nown : c);
-                        p = __dmul_rn(vv[u], halo ? ld_halo_f64(src) : ld_gather_f64(src, pl));
+                        p = __dmul_rn(vv[u], halo ? ld_halo_f64(src, pl) : ld_gather_f64(src, pl));
                     }
                     prod[jj * 32 + lane] = p;
                 }
@@ -125,7 +122,47 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
         const int64_t row = sell_row(A, s * 32 + lane);
         if (row >= 0) epi(row, sum);
     }
+}
+
+template <class Epi, int MODE, int NW, int U>
+__global__ void __launch_bounds__(NW * 32)
+k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
+    __shared__ double prod[SPLIT_CHUNK * 32];
+    const double *xh = A.xh;
+    if (MODE == ROWS_GEN) xh = halo_wait(A);
+    split_rows_body<Epi, MODE, NW, U>(A, blockIdx.x, xg, xh, epi, prod);
     if (MODE == ROWS_GEN && A.complete) halo_complete(A, gridDim.x);
+}
+
+// Interior and boundary slices of a distributed matrix (p2p transport) in ONE
+// launch: CTAs [0, ncta_i) take the interior view I (no halo column), the
+// rest the boundary view B, which waits for the halo in-kernel and completes
+// the exchange.  The boundary CTAs are the last ones dispatched, so the pack
+// kernels have had the whole interior to land, and they fill the interior's
+// tail wave instead of running as a second, dependent launch.
+template <class Epi, int IMODE>
+__global__ void __launch_bounds__(ROWS_BLOCK, 8)
+k_thread_rows_fused(SellView I, SellView B, int64_t ncta_i, const double *__restrict__ xg, Epi epi) {
+    if ((int64_t)blockIdx.x < ncta_i) {  // IMODE: ROWS_PLAIN (run table) or ROWS_GEN (slice list)
+        thread_rows_body<Epi, IMODE, false>(I, blockIdx.x, xg, nullptr, epi);
+    } else {
+        const double *xh = halo_wait(B);
+        thread_rows_body<Epi, ROWS_GEN, true>(B, blockIdx.x - ncta_i, xg, xh, epi);
+        halo_complete(B, gridDim.x - (unsigned)ncta_i);
+    }
+}
+
+template <class Epi, int NW, int U>
+__global__ void __launch_bounds__(NW * 32)
+k_split_rows_fused(SellView I, SellView B, int64_t ncta_i, const double *__restrict__ xg, Epi epi) {
+    __shared__ double prod[SPLIT_CHUNK * 32];
+    if ((int64_t)blockIdx.x < ncta_i) {
+        split_rows_body<Epi, ROWS_GEN, NW, U>(I, blockIdx.x, xg, nullptr, epi, prod);
+    } else {
+        const double *xh = halo_wait(B);
+        split_rows_body<Epi, ROWS_GEN, NW, U>(B, blockIdx.x - ncta_i, xg, xh, epi, prod);
+        halo_complete(B, gridDim.x - (unsigned)ncta_i);
+    }
 }
 
 // Schedule choice, per launch: split when rows are long and the launch has
@@ -236,6 +273,53 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     v.xh = nullptr;
     const int nrecvp = v.nrecvp;
     v.nrecvp = 0;
+    // one launch over interior + boundary slices (k_*_rows_fused) where it
+    // measured faster (tools/dist_levels.py, 4 GPUs, profiles/r02_halo_fuse.md):
+    // coarse levels and long rows; the fine level's short rows (7-point A,
+    // P) ran 8 % slower fused and keep the two launches
+    const bool fuse = ctx->halo_fuse == 2 ||
+                      (ctx->halo_fuse == 1 && (A->nslices < (1 << 18) || A->max_width >= 16));
+    if (p2p && h.n_boundary > 0 && h.n_interior > 0 && fuse) {
+        // the wait for the local pack kernel (it reads xg) follows the launch
+        SellView b = v;
+        auto set_list = [&](SellView &w, const std::vector<std::pair<int64_t, int64_t>> &runs,
+                            const int32_t *list, int64_t n) {
+            if (runs.size() <= SELL_RUNS) {
+                w.slist = nullptr;
+                w.nruns = (int)runs.size();
+                int64_t end = 0;
+                for (size_t r = 0; r < runs.size(); r++) {
+                    w.run_s0[r] = runs[r].first;
+                    end += runs[r].second;
+                    w.run_end[r] = end;
+                }
+                w.nlist = end;
+            } else {
+                w.slist = list;
+                w.nlist = n;
+            }
+        };
+        set_list(v, h.interior_runs, h.interior, h.n_interior);
+        set_list(b, h.boundary_runs, h.boundary, h.n_boundary);
+        b.nown = h.nown;
+        b.xh = h.halo;
+        b.xh_stride = h.nhalo;
+        b.nrecvp = nrecvp;
+        b.complete = 1;
+        if (Epi::kSpmv && use_split(A, v.nlist + b.nlist)) {
+            k_split_rows_fused<Epi, SPLIT_WARPS, SPLIT_U>
+                <<<(unsigned)(v.nlist + b.nlist), SPLIT_WARPS * 32, 0, cur_stream(ctx)>>>(v, b, v.nlist, xg, epi);
+        } else {
+            const int64_t ci = (v.nlist + ROWS_SLICES - 1) / ROWS_SLICES;
+            const int64_t cb = (b.nlist + ROWS_SLICES - 1) / ROWS_SLICES;
+            if (v.slist)
+                k_thread_rows_fused<Epi, ROWS_GEN><<<(unsigned)(ci + cb), ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, b, ci, xg, epi);
+            else
+                k_thread_rows_fused<Epi, ROWS_PLAIN><<<(unsigned)(ci + cb), ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, b, ci, xg, epi);
+        }
+        AMGP_CHECK_LAUNCH(ctx);
+        return halo_exchange_end(ctx, A);
+    }
     AMGP_TRY(launch_set(h.interior_runs, h.interior, h.n_interior));
     AMGP_TRY(halo_exchange_end(ctx, A));
     v.nown = h.nown;

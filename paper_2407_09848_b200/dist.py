@@ -303,7 +303,7 @@ class DistHierarchy:
     """This rank's slice of an AMG hierarchy on its GPU (libamgp hierarchy
     with halo-exchanging matrices).  Vectors are the rank's fine-level rows."""
 
-    def __init__(self, d, comm, smoother, replicate_below=20000, coarse_sweeps=None, use_graph=False,
+    def __init__(self, d, comm, smoother, replicate_below=20000, coarse_sweeps=None, use_graph=True,
                  coarse_solver=None):
         """Partition a shared global hierarchy (share_hierarchy) by rows."""
         c = comm.ctx
@@ -341,7 +341,7 @@ class DistHierarchy:
         self.plans = plans
 
     @classmethod
-    def from_levels(cls, levels, comm, smoother, coarse_solver="l1_jacobi", coarse_sweeps=30, use_graph=False):
+    def from_levels(cls, levels, comm, smoother, coarse_solver="l1_jacobi", coarse_sweeps=30, use_graph=True):
         """Hierarchy from the per-rank levels of the distributed device setup
         (dsetup.build_levels)."""
         self = cls.__new__(cls)

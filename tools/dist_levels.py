@@ -26,6 +26,7 @@ def main():
     ap.add_argument("--reps", type=int, default=20)
     ap.add_argument("--family", default="opt_cheb4")
     ap.add_argument("--k", type=int, default=4)
+    ap.add_argument("--no-solve", action="store_true", help="skip the PCG solve (AMGP_HALO_NOSYNC experiments)")
     ap.add_argument("--per-rank", action="store_true",
                     help="also: per-rank rows / nnz of levels >= 1 and their SpMV time without the exchange")
     args = ap.parse_args()
@@ -159,6 +160,13 @@ def main():
             return dh.solve(b, cfg=kc)
         return P.solve(D0, b, precond=P.as_vcycle_preconditioner(h), cfg=kc)
 
+    if args.no_solve:
+        if rank == 0:
+            print(json.dumps(out), flush=True)
+        if ws > 1:
+            dist.barrier()
+            dist.destroy_process_group()
+        return
     run()
     ts = []
     for _ in range(3):

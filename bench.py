@@ -583,8 +583,27 @@ def run_b200(args):
         t = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e2e_s = float(t.item())
+    # the e2e bound: this box's pinned host -> device copy rate (the H2D
+    # stream carries 2/3 of the copied bytes and is never idle in the pipeline)
+    h2d_bytes = len(cfgs) * 2 * n * 8
+    hb = torch.empty(n, dtype=torch.float64, pin_memory=True)
+    db = torch.empty(n, dtype=torch.float64, device="cuda")
+    db.copy_(hb, non_blocking=True)
+    torch.cuda.synchronize()
+    c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    c0.record()
+    for _ in range(8):
+        db.copy_(hb, non_blocking=True)
+    c1.record()
+    torch.cuda.synchronize()
+    h2d_gbs = 8 * n * 8 / (c0.elapsed_time(c1) * 1e-3) / 1e9
+    del hb, db
+    e2e_bound = job_step_bytes / (h2d_bytes / (h2d_gbs * 1e9)) / 1e9
     e2e = {"value": job_step_bytes / e2e_s / 1e9, "unit": "GB/s",
-           "h2d_bytes_per_step": len(cfgs) * 2 * n * 8, "d2h_bytes_per_step": len(cfgs) * n * 8,
+           "h2d_bytes_per_step": h2d_bytes, "d2h_bytes_per_step": len(cfgs) * n * 8,
+           "h2d_GBs_measured": h2d_gbs, "bound_GBs": e2e_bound,
+           "frac_of_bound": job_step_bytes / e2e_s / 1e9 / e2e_bound,
+           "bound": "pinned H2D copy rate of this GPU (measured here): h2d_bytes_per_step / rate",
            "api": "smoother_apply_batch (amgp_smoother_apply_host): per-apply H2D of b, x0 and D2H of x, "
                   "pipelined across the 18 applies", "bitwise_vs_device_call": e2e_bitwise}
 

@@ -1,6 +1,7 @@
 #!/usr/bin/env python
 """A/B of solve time between library builds in ONE process series on one box:
     python tools/ab_solve.py --m 128 --libs a.so b.so --rounds 4
+    python tools/ab_solve.py --m 128 --libs AMGP_PDL=0 AMGP_PDL=1   (env settings instead of builds)
 Each round runs every lib in a fresh subprocess (median of 7 solves)."""
 import argparse, json, os, subprocess, sys
 REPO = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
@@ -33,7 +34,10 @@ res = {l: [] for l in a.libs}
 for r in range(a.rounds):
     for l in a.libs:
         env = dict(os.environ)
-        if l != "default":
+        if "=" in l:
+            k, v = l.split("=", 1)
+            env[k] = v
+        elif l != "default":
             env["AMGP_LIB"] = l
         out = subprocess.run([sys.executable, "-c", CHILD, REPO, str(a.m), a.family], capture_output=True, text=True, env=env)
         line = [x for x in out.stdout.splitlines() if x.startswith("{")]

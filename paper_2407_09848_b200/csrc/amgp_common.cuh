@@ -78,6 +78,9 @@ struct amgp_ctx {
     // p2p: interior and boundary slices in one launch (rows.cuh launch_rows):
     // AMGP_HALO_FUSE=0 never, 1 where it measured faster (default), 2 always
     int halo_fuse = 1;
+    // fused launches also pack the halo in their first CTAs (no pack kernel,
+    // no cross-stream events); AMGP_HALO_XPACK=0: the separate pack kernel
+    int halo_xpack = 1;
     // copy streams of the host-buffer smoother path (created on first use)
     cudaStream_t io_h2d = nullptr, io_d2h = nullptr;
     unsigned long long *sync = nullptr;            // [AMGP_MAX_SLOTS][sync_stride]
@@ -307,6 +310,55 @@ __device__ __forceinline__ void halo_complete(const SellView &A, unsigned nctas)
         }
     }
 }
+
+// p2p pack of one exchange (the k_pack_p2p kernel, and the first CTAs of the
+// fused row kernels, rows.cuh): entry i of the send list goes straight to its
+// receiver's halo buffer of this exchange's parity; ncta CTAs share the list
+// and the last of them publishes ready = epoch + 1 on every receiver.  Before
+// writing, a non-symmetric exchange waits until each receiver consumed
+// exchange epoch - 2 (see dist.cu).
+struct PackView {
+    int64_t n = 0;  // entries to send
+    int npeers = 0, nsendp = 0, sym = 1;
+    const int64_t *idx = nullptr;
+    double *const *dest = nullptr;  // [2 npeers]
+    const int64_t *seg = nullptr;   // [npeers + 1]
+    const int *sendp = nullptr;
+    unsigned long long *const *ready_remote = nullptr;
+};
+
+__device__ __forceinline__ void halo_pack(const PackView &pk, unsigned long long *sync, int nranks,
+                                          const double *__restrict__ x, int64_t cta, int64_t ncta) {
+    const unsigned long long epoch = ld_relaxed_gpu(sync + 2 * nranks);
+    if (!pk.sym && epoch >= 2) {
+        if (threadIdx.x == 0) {  // relaxed polls, one acquire (an acquire load invalidates the SM's L1)
+            for (int i = 0; i < pk.nsendp; i++) {
+                const unsigned long long *w = sync + nranks + pk.sendp[i];
+                while (ld_relaxed_sys(w) + 1 < epoch) __nanosleep(20);
+                (void)ld_acquire_sys(w);
+            }
+        }
+        __syncthreads();
+    }
+    const int par = (int)(epoch & 1ull);
+    for (int64_t i = cta * blockDim.x + threadIdx.x; i < pk.n; i += ncta * blockDim.x) {
+        int q = 0;
+        while (q + 1 < pk.npeers && i >= pk.seg[q + 1]) q++;
+        pk.dest[par * pk.npeers + q][i - pk.seg[q]] = x[pk.idx[i]];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence_system();
+        unsigned long long *ticket = sync + 2 * nranks + 1;
+        if (atomicAdd(ticket, 1ull) == (unsigned long long)ncta - 1) {
+            *ticket = 0;
+            __threadfence_system();
+            for (int i = 0; i < pk.nsendp; i++) st_release_sys(pk.ready_remote[i], epoch + 1);
+        }
+    }
+}
+
+PackView pack_view(const HaloPlan &h);  // dist.cu
 
 // Exchange the halo of operand x (own part) for a distributed matrix; after
 // it, kernels may gather x through view.xh (dist.cu).

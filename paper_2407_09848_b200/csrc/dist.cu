@@ -160,6 +160,8 @@ static int p2p_init(amgp_ctx *ctx) {
     ctx->halo_p2p = 1;
     const char *fz = getenv("AMGP_HALO_FUSE");
     ctx->halo_fuse = fz && fz[0] >= '0' && fz[0] <= '2' ? fz[0] - '0' : 1;
+    const char *xp = getenv("AMGP_HALO_XPACK");
+    ctx->halo_xpack = !(xp && xp[0] == '0');
     return AMGP_OK;
 }
 
@@ -432,41 +434,25 @@ __global__ void k_pack(int64_t n, const int64_t *__restrict__ idx, const double 
 // buffer e & 1, so it only has to wait until each receiver has consumed
 // exchange e - 2 -- and not at all when every receiver also sends to me: my
 // launches of exchange e - 1 waited for its pack of e - 1, which its stream
-// issued after its boundary launch of e - 2).  The last CTA to finish
-// publishes the new epoch.
-__global__ void k_pack_p2p(int64_t n, int npeers, const int64_t *__restrict__ idx,
-                           const double *__restrict__ x, double *const *__restrict__ dest,
-                           const int64_t *__restrict__ seg, unsigned long long *sync, int nranks,
-                           const int *__restrict__ sendp, int nsendp, int sym,
-                           unsigned long long *const *__restrict__ ready_remote) {
-    const unsigned long long epoch = ld_relaxed_gpu(sync + 2 * nranks);
-    if (!sym && epoch >= 2) {
-        if (threadIdx.x == 0) {  // relaxed polls, one acquire (an acquire load invalidates the SM's L1)
-            for (int i = 0; i < nsendp; i++) {
-                const unsigned long long *w = sync + nranks + sendp[i];
-                while (ld_relaxed_sys(w) + 1 < epoch) __nanosleep(20);
-                (void)ld_acquire_sys(w);
-            }
-        }
-        __syncthreads();
-    }
-    const int par = (int)(epoch & 1ull);
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        int q = 0;
-        while (q + 1 < npeers && i >= seg[q + 1]) q++;
-        dest[par * npeers + q][i - seg[q]] = x[idx[i]];
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        __threadfence_system();
-        unsigned long long *ticket = sync + 2 * nranks + 1;
-        if (atomicAdd(ticket, 1ull) == gridDim.x - 1) {
-            *ticket = 0;
-            __threadfence_system();
-            for (int i = 0; i < nsendp; i++) st_release_sys(ready_remote[i], epoch + 1);
-        }
-    }
+// issued after its boundary launch of e - 2; with the pack inside the fused
+// row kernel: its kernel of e - 1, boundary included, completed before its
+// kernel of e started).  The last CTA to finish publishes the new epoch.
+__global__ void k_pack_p2p(PackView pk, const double *__restrict__ x, unsigned long long *sync, int nranks) {
+    halo_pack(pk, sync, nranks, x, blockIdx.x, gridDim.x);
+}
+
+PackView pack_view(const HaloPlan &h) {
+    PackView pk;
+    pk.n = h.nsend;
+    pk.npeers = (int)h.peers.size();
+    pk.idx = h.send_idx;
+    pk.dest = h.d_dest;
+    pk.seg = h.d_seg;
+    pk.sendp = h.d_sendp;
+    pk.nsendp = h.nsendp;
+    pk.sym = (int)h.sym;
+    pk.ready_remote = h.d_ready_remote;
+    return pk;
 }
 
 // after the boundary rows: this exchange is complete on this rank
@@ -495,10 +481,7 @@ static int p2p_begin(amgp_ctx *ctx, const HaloPlan &h, const double *x) {
     attr[0].val.priority = ctx->prio_high;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
-    AMGP_CUDA(cudaLaunchKernelEx(&cfg, k_pack_p2p, h.nsend, (int)h.peers.size(), (const int64_t *)h.send_idx,
-                                 (const double *)x, (double *const *)h.d_dest, (const int64_t *)h.d_seg,
-                                 h.sync_slot, ctx->nranks, (const int *)h.d_sendp, h.nsendp, (int)h.sym,
-                                 (unsigned long long *const *)h.d_ready_remote));
+    AMGP_CUDA(cudaLaunchKernelEx(&cfg, k_pack_p2p, pack_view(h), (const double *)x, h.sync_slot, ctx->nranks));
     AMGP_CHECK_LAUNCH(ctx);
     AMGP_CUDA(cudaEventRecord(ctx->ev_exchanged, ctx->comm_stream));
     return AMGP_OK;

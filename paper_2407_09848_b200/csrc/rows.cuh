@@ -135,33 +135,49 @@ k_split_rows(SellView A, const double *__restrict__ xg, Epi epi) {
 }
 
 // Interior and boundary slices of a distributed matrix (p2p transport) in ONE
-// launch: CTAs [0, ncta_i) take the interior view I (no halo column), the
-// rest the boundary view B, which waits for the halo in-kernel and completes
-// the exchange.  The boundary CTAs are the last ones dispatched, so the pack
-// kernels have had the whole interior to land, and they fill the interior's
-// tail wave instead of running as a second, dependent launch.
+// launch: CTAs [0, ncta_p) pack this exchange's halo for the peers (halo_pack;
+// ncta_p = 0 when a separate pack kernel does it), then ncta_i CTAs take the
+// interior view I (no halo column), the rest the boundary view B, which waits
+// for the peers' halo in-kernel.  Packing CTAs come first and wait for nothing
+// of this exchange, so every rank's pack makes progress; the boundary CTAs are
+// the last ones dispatched, so the peers' stores have had the whole interior
+// to land, and they fill the interior's tail wave instead of running as a
+// second, dependent launch.  Pack and boundary CTAs all arrive on the
+// completion ticket: the last one advances the epoch.
 template <class Epi, int IMODE>
 __global__ void __launch_bounds__(ROWS_BLOCK, 8)
-k_thread_rows_fused(SellView I, SellView B, int64_t ncta_i, const double *__restrict__ xg, Epi epi) {
-    if ((int64_t)blockIdx.x < ncta_i) {  // IMODE: ROWS_PLAIN (run table) or ROWS_GEN (slice list)
-        thread_rows_body<Epi, IMODE, false>(I, blockIdx.x, xg, nullptr, epi);
+k_thread_rows_fused(SellView I, SellView B, PackView pk, int64_t ncta_p, int64_t ncta_i,
+                    const double *__restrict__ xg, Epi epi) {
+    const int64_t b = blockIdx.x;
+    const unsigned ndone = gridDim.x - (unsigned)ncta_i;
+    if (b < ncta_p) {
+        halo_pack(pk, B.sync_slot, B.nranks, xg, b, ncta_p);
+        halo_complete(B, ndone);
+    } else if (b < ncta_p + ncta_i) {  // IMODE: ROWS_PLAIN (run table) or ROWS_GEN (slice list)
+        thread_rows_body<Epi, IMODE, false>(I, b - ncta_p, xg, nullptr, epi);
     } else {
         const double *xh = halo_wait(B);
-        thread_rows_body<Epi, ROWS_GEN, true>(B, blockIdx.x - ncta_i, xg, xh, epi);
-        halo_complete(B, gridDim.x - (unsigned)ncta_i);
+        thread_rows_body<Epi, ROWS_GEN, true>(B, b - ncta_p - ncta_i, xg, xh, epi);
+        halo_complete(B, ndone);
     }
 }
 
 template <class Epi, int NW, int U>
 __global__ void __launch_bounds__(NW * 32)
-k_split_rows_fused(SellView I, SellView B, int64_t ncta_i, const double *__restrict__ xg, Epi epi) {
+k_split_rows_fused(SellView I, SellView B, PackView pk, int64_t ncta_p, int64_t ncta_i,
+                   const double *__restrict__ xg, Epi epi) {
     __shared__ double prod[SPLIT_CHUNK * 32];
-    if ((int64_t)blockIdx.x < ncta_i) {
-        split_rows_body<Epi, ROWS_GEN, NW, U>(I, blockIdx.x, xg, nullptr, epi, prod);
+    const int64_t b = blockIdx.x;
+    const unsigned ndone = gridDim.x - (unsigned)ncta_i;
+    if (b < ncta_p) {
+        halo_pack(pk, B.sync_slot, B.nranks, xg, b, ncta_p);
+        halo_complete(B, ndone);
+    } else if (b < ncta_p + ncta_i) {
+        split_rows_body<Epi, ROWS_GEN, NW, U>(I, b - ncta_p, xg, nullptr, epi, prod);
     } else {
         const double *xh = halo_wait(B);
-        split_rows_body<Epi, ROWS_GEN, NW, U>(B, blockIdx.x - ncta_i, xg, xh, epi, prod);
-        halo_complete(B, gridDim.x - (unsigned)ncta_i);
+        split_rows_body<Epi, ROWS_GEN, NW, U>(B, b - ncta_p - ncta_i, xg, xh, epi, prod);
+        halo_complete(B, ndone);
     }
 }
 
@@ -216,7 +232,16 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     const bool p2p = ctx->halo_p2p > 0;
     if (A->nslices == 0 && !p2p) return AMGP_OK;
     SellView v = view_of(A);
-    AMGP_TRY(halo_exchange_begin(ctx, A, xg));
+    // one launch over interior + boundary slices (k_*_rows_fused) where it
+    // measured faster (tools/dist_levels.py, 4 GPUs, profiles/r02_halo_fuse.md):
+    // coarse levels and long rows (the fine level's short rows ran 8 % slower
+    // fused next to a separate pack kernel); with halo_xpack the fused launch
+    // packs the halo itself (no pack kernel, no cross-stream events)
+    const bool fuse = p2p && A->nslices >= 2 * 148 && h.n_boundary > 0 && h.n_interior > 0 &&
+                      (ctx->halo_fuse == 2 ||
+                       (ctx->halo_fuse == 1 && (A->nslices < (1 << 18) || A->max_width >= 16)));
+    const bool xpack = fuse && ctx->halo_xpack;
+    if (!xpack) AMGP_TRY(halo_exchange_begin(ctx, A, xg));
     if (p2p) {
         v.sync_slot = h.sync_slot;
         v.recvp = h.d_recvp;
@@ -273,14 +298,8 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     v.xh = nullptr;
     const int nrecvp = v.nrecvp;
     v.nrecvp = 0;
-    // one launch over interior + boundary slices (k_*_rows_fused) where it
-    // measured faster (tools/dist_levels.py, 4 GPUs, profiles/r02_halo_fuse.md):
-    // coarse levels and long rows; the fine level's short rows (7-point A,
-    // P) ran 8 % slower fused and keep the two launches
-    const bool fuse = ctx->halo_fuse == 2 ||
-                      (ctx->halo_fuse == 1 && (A->nslices < (1 << 18) || A->max_width >= 16));
-    if (p2p && h.n_boundary > 0 && h.n_interior > 0 && fuse) {
-        // the wait for the local pack kernel (it reads xg) follows the launch
+    if (fuse) {
+        // separate pack kernel: the wait for it (it reads xg) follows the launch
         SellView b = v;
         auto set_list = [&](SellView &w, const std::vector<std::pair<int64_t, int64_t>> &runs,
                             const int32_t *list, int64_t n) {
@@ -306,19 +325,25 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
         b.xh_stride = h.nhalo;
         b.nrecvp = nrecvp;
         b.complete = 1;
+        PackView pk;
+        if (xpack) pk = pack_view(h);
         if (Epi::kSpmv && use_split(A, v.nlist + b.nlist)) {
+            const int64_t cp = xpack && h.nsend > 0 ? std::min<int64_t>(grid_for(h.nsend, SPLIT_WARPS * 32), 148) : 0;
             k_split_rows_fused<Epi, SPLIT_WARPS, SPLIT_U>
-                <<<(unsigned)(v.nlist + b.nlist), SPLIT_WARPS * 32, 0, cur_stream(ctx)>>>(v, b, v.nlist, xg, epi);
+                <<<(unsigned)(cp + v.nlist + b.nlist), SPLIT_WARPS * 32, 0, cur_stream(ctx)>>>(v, b, pk, cp, v.nlist,
+                                                                                               xg, epi);
         } else {
+            const int64_t cp = xpack && h.nsend > 0 ? std::min<int64_t>(grid_for(h.nsend, ROWS_BLOCK), 148) : 0;
             const int64_t ci = (v.nlist + ROWS_SLICES - 1) / ROWS_SLICES;
             const int64_t cb = (b.nlist + ROWS_SLICES - 1) / ROWS_SLICES;
+            const unsigned g = (unsigned)(cp + ci + cb);
             if (v.slist)
-                k_thread_rows_fused<Epi, ROWS_GEN><<<(unsigned)(ci + cb), ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, b, ci, xg, epi);
+                k_thread_rows_fused<Epi, ROWS_GEN><<<g, ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, b, pk, cp, ci, xg, epi);
             else
-                k_thread_rows_fused<Epi, ROWS_PLAIN><<<(unsigned)(ci + cb), ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, b, ci, xg, epi);
+                k_thread_rows_fused<Epi, ROWS_PLAIN><<<g, ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, b, pk, cp, ci, xg, epi);
         }
         AMGP_CHECK_LAUNCH(ctx);
-        return halo_exchange_end(ctx, A);
+        return xpack ? AMGP_OK : halo_exchange_end(ctx, A);
     }
     AMGP_TRY(launch_set(h.interior_runs, h.interior, h.n_interior));
     AMGP_TRY(halo_exchange_end(ctx, A));

@@ -249,28 +249,29 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
         v.nranks = ctx->nranks;
         v.consumed_remote = h.d_consumed_remote;
     }
-    auto set_runs = [&](const std::vector<std::pair<int64_t, int64_t>> &runs) {
-        v.slist = nullptr;
-        v.nruns = (int)runs.size();
-        int64_t end = 0;
-        for (size_t r = 0; r < runs.size(); r++) {
-            v.run_s0[r] = runs[r].first;
-            end += runs[r].second;
-            v.run_end[r] = end;
+    // a set of at most SELL_RUNS contiguous runs is launched over the run
+    // table (no slice-list indirection), else over the list
+    auto set_list = [](SellView &w, const std::vector<std::pair<int64_t, int64_t>> &runs, const int32_t *list,
+                       int64_t n) {
+        if (runs.size() <= SELL_RUNS) {
+            w.slist = nullptr;
+            w.nruns = (int)runs.size();
+            int64_t end = 0;
+            for (size_t r = 0; r < runs.size(); r++) {
+                w.run_s0[r] = runs[r].first;
+                end += runs[r].second;
+                w.run_end[r] = end;
+            }
+            w.nlist = end;
+        } else {
+            w.slist = list;
+            w.nlist = n;
         }
-        v.nlist = end;
     };
-    // a set of at most SELL_RUNS contiguous runs is one launch over the run
-    // table (no slice-list indirection), else one launch over the list
     auto launch_set = [&](const std::vector<std::pair<int64_t, int64_t>> &runs,
                           const int32_t *list, int64_t n) -> int {
         if (n == 0) return AMGP_OK;
-        if (runs.size() <= SELL_RUNS) {
-            set_runs(runs);
-        } else {
-            v.slist = list;
-            v.nlist = n;
-        }
+        set_list(v, runs, list, n);
         return launch_view(ctx, A, v, xg, epi);
     };
     // a matrix with fewer slices than two per SM is launch-latency bound:
@@ -299,25 +300,7 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
     const int nrecvp = v.nrecvp;
     v.nrecvp = 0;
     if (fuse) {
-        // separate pack kernel: the wait for it (it reads xg) follows the launch
         SellView b = v;
-        auto set_list = [&](SellView &w, const std::vector<std::pair<int64_t, int64_t>> &runs,
-                            const int32_t *list, int64_t n) {
-            if (runs.size() <= SELL_RUNS) {
-                w.slist = nullptr;
-                w.nruns = (int)runs.size();
-                int64_t end = 0;
-                for (size_t r = 0; r < runs.size(); r++) {
-                    w.run_s0[r] = runs[r].first;
-                    end += runs[r].second;
-                    w.run_end[r] = end;
-                }
-                w.nlist = end;
-            } else {
-                w.slist = list;
-                w.nlist = n;
-            }
-        };
         set_list(v, h.interior_runs, h.interior, h.n_interior);
         set_list(b, h.boundary_runs, h.boundary, h.n_boundary);
         b.nown = h.nown;
@@ -343,6 +326,7 @@ int launch_rows(amgp_ctx *ctx, const amgp_mat *A, const double *xg, const Epi &e
                 k_thread_rows_fused<Epi, ROWS_PLAIN><<<g, ROWS_BLOCK, 0, cur_stream(ctx)>>>(v, b, pk, cp, ci, xg, epi);
         }
         AMGP_CHECK_LAUNCH(ctx);
+        // a separate pack kernel reads xg: later work on this stream waits for it
         return xpack ? AMGP_OK : halo_exchange_end(ctx, A);
     }
     AMGP_TRY(launch_set(h.interior_runs, h.interior, h.n_interior));

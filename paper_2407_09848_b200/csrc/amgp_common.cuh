@@ -87,6 +87,13 @@ struct amgp_ctx {
     std::vector<unsigned long long *> peer_sync;   // every rank's sync array (self included)
     int sync_stride = 0;
     int next_slot = 0;
+    // p2p ordered all-reduce (dist.cu allreduce_sum_ordered): a region after
+    // the slots of every rank's sync array, [2 parities][nranks][32 words]
+    // (16 values, word 31 = the sender's epoch flag), then a local epoch word
+    unsigned long long *red = nullptr;                   // my region
+    unsigned long long *const *d_peer_red = nullptr;     // device [nranks]: every rank's region
+    unsigned long long *red_epoch = nullptr;
+    int red_ar = 1;  // AMGP_P2P_ALLREDUCE=0: NCCL AllGather + fold instead
 };
 
 // Slots are never reused: a freed slot's words may still receive a peer's

@@ -652,9 +652,12 @@ def run_b200(args):
                          "frac": achieved / peak, "peak_kind": peak_kind,
                          "kernel": "k_thread_rows<Cheb4Step<0,0,0>,0> (cheb4 middle degree step)",
                          "bytes_per_launch": mb, "ms_per_launch": t_mid,
-                         "traffic": (traffic or {}).get("bytes_per_launch"),
+                         # the static capture is of the 256^3 single-GPU kernel: other sizes get null
+                         "traffic": (traffic or {}).get("bytes_per_launch") if (m == 256 and ws == 1) else None,
                          "traffic_source": "static: ncu --set full capture of this kernel at 256^3, "
-                                           "profiles/ncu_traffic.json (not measured in this run)"},
+                                           "profiles/ncu_traffic.json (not measured in this run)"
+                                           if (m == 256 and ws == 1) else
+                                           "none: the static ncu capture is of the 256^3 single-GPU kernel"},
             "mid_step_ms": mids,
             "apply_ms": {f"{f}_k{k}": v for (f, k), v in t_apply.items()},
             "e2e": e2e,

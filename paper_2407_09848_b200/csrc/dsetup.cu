@@ -131,11 +131,15 @@ __global__ void k_ds_scale(int64_t n, const double *__restrict__ w, const double
 //
 // The chains are latency bound (one dependent FMA per 32 elements per lane),
 // so the operands are staged by the bulk-copy engine: one producer thread
-// issues cp.async.bulk copies of x and y into an 8-stage shared-memory ring
+// issues cp.async.bulk copies of x and y into a 12-stage shared-memory ring
 // (mbarrier complete_tx), the consumer warp runs the chains out of shared
 // memory.  Misaligned chunks take the plain-load path (same arithmetic).
-#define DOT_STAGES 8
+#ifndef DOT_STAGES
+#define DOT_STAGES 12  // 192 KB in flight for the one-SM chain (8: 128 KB; tools/setup_ab.py, same bits)
+#endif
+#ifndef DOT_CH
 #define DOT_CH 1024  // doubles per stage per operand (8 KB)
+#endif
 
 __device__ __forceinline__ uint32_t smem_u32(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
